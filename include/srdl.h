@@ -1,0 +1,181 @@
+/*
+ * srdl.h — C ABI of the sm_100a semi-naive fixpoint library (libsrdl.so).
+ *
+ * This is the drop-in boundary under the reference's Python API: every
+ * numeric operation the reference evaluates with numpy on the host
+ * (pkg/src/flatlog/rowops.py, storage.py, executor.py) has exactly one entry
+ * point here, taking plain device pointers, row counts and a CUDA stream.
+ * No torch types cross this boundary; a ctypes (or cgo/JNI) binding can call
+ * it directly. See INTEGRATION.md for the reference-side binding.
+ *
+ * Conventions
+ *   - Relations are Structure-of-Arrays: `arity` device arrays of uint32 ids,
+ *     rows sorted lexicographically over the columns in index order.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Every function returns 0 on success and a negative code on error;
+ *     srdl_last_error() gives the message (thread-local).
+ *   - Host-side counts written through `uint64_t *n_out` require a stream
+ *     synchronisation, which the function performs (two-phase allocation:
+ *     the caller sizes the next buffer from that count).
+ *   - Scratch memory comes from the device's stream-ordered memory pool.
+ */
+#ifndef SRDL_H
+#define SRDL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRDL_VERSION 1
+#define SRDL_MAX_ATOMS 12   /* body atoms per rule instance        */
+#define SRDL_MAX_LEVELS 12  /* variables per rule instance         */
+#define SRDL_MAX_COLS 8     /* columns per atom                    */
+#define SRDL_MAX_HEAD 12    /* head arity                          */
+#define SRDL_MAX_SEGS 2     /* body + head buffer of one index     */
+#define SRDL_NO_ATOM 255u
+#define SRDL_NO_SYMBOL 0xFFFFFFFFu
+
+#define SRDL_OK 0
+#define SRDL_ERR_CUDA -1
+#define SRDL_ERR_ARG -2
+#define SRDL_ERR_INTERNAL -3
+
+/* ------------------------------------------------------------------ misc */
+
+int srdl_version(void);
+const char *srdl_last_error(void);
+/* Number of SMs of the current device (grid sizing), or a negative code. */
+int srdl_sm_count(void);
+/* Kernels launched by this library since load (process-wide counter). */
+uint64_t srdl_launch_count(void);
+
+/* --------------------------------------------------------------- storage
+ * reference: rowops.sort_dedup (rowops.py:60) / storage.sort_dedup
+ * (storage.py:304). Sorts n rows of `arity` columns lexicographically and
+ * removes duplicates. `bits` = significant bits per id (ceil(log2(#symbols)),
+ * at most 32): columns are radix-sorted on packed keys of bits*arity bits.
+ * out: `arity` arrays with capacity n. *n_out = distinct rows (host). */
+int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                    uint32_t *const *out, uint64_t *n_out, void *stream);
+
+/* reference: storage.compute_delta (storage.py:311): distinct staged rows
+ * minus the rows of up to two sorted, duplicate-free segments of the full
+ * relation (head and body). Fuses sort, unique and the anti-join.
+ * seg_cols[s] points to `arity` column pointers of segment s. */
+int srdl_compute_delta(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                       const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,
+                       uint32_t nseg, uint32_t *const *out, uint64_t *n_out, void *stream);
+
+/* reference: rowops.merge_sorted (rowops.py:77) and the single-pass
+ * head->body flush of ColumnarRelation.merge_delta (storage.py:272).
+ * Merges two sorted, mutually disjoint row sets into out (na+nb rows). */
+int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, uint64_t nb,
+               uint32_t arity, uint32_t *const *out, void *stream);
+
+/* reference: rowops.is_sorted_strict (rowops.py:64). *ok = 1 iff rows are
+ * strictly increasing (sorted, no duplicates). */
+int srdl_is_sorted_strict(const uint32_t *const *cols, uint32_t arity, uint64_t n, int *ok,
+                          void *stream);
+
+/* Gather rows: out[c][i] = cols[c][idx[i]] (index builds, column permutes). */
+int srdl_gather(const uint32_t *const *cols, uint32_t arity, const uint32_t *idx, uint64_t n,
+                uint32_t *const *out, void *stream);
+
+/* ------------------------------------------------------------ histograms
+ * reference: storage.Histogram.over_column (storage.py:48). Run-length of a
+ * sorted column: keys[K], degrees[K], inclusive prefix[K] (uint64).
+ * keys/degrees/prefix have capacity n; *k_out = K (host). */
+int srdl_histogram(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *degrees,
+                   uint64_t *prefix, uint64_t *k_out, void *stream);
+
+/* reference: storage.Histogram.updated (storage.py:63): union of two
+ * histograms, degrees of equal keys added. Outputs have capacity na+nb. */
+int srdl_histogram_merge(const uint32_t *ka, const uint32_t *da, uint64_t na, const uint32_t *kb,
+                         const uint32_t *db, uint64_t nb, uint32_t *keys, uint32_t *degrees,
+                         uint64_t *prefix, uint64_t *k_out, void *stream);
+
+/* Narrow one sorted segment on its leading columns to constant values
+ * (reference: executor.prepare constant narrowing, executor.py:188-206,
+ * storage.narrow_segments, storage.py:122). Returns [*lo, *hi) on the host. */
+int srdl_narrow_prefix(const uint32_t *const *cols, uint64_t n, const uint32_t *values,
+                       uint32_t nvalues, uint64_t *lo, uint64_t *hi, void *stream);
+
+/* ------------------------------------------------------------------ WCOJ */
+
+typedef struct {
+    const uint32_t *cols[SRDL_MAX_COLS]; /* index-order columns        */
+    uint32_t lo, hi;                     /* rows left after constants  */
+} srdl_segment;
+
+typedef struct {
+    srdl_segment seg[SRDL_MAX_SEGS];
+    uint32_t nseg;
+    uint32_t negated;
+    uint32_t arity;
+    uint32_t nconst;
+    int32_t check_level;                 /* negated: level of the probe, else -1 */
+    uint8_t lvl_col[SRDL_MAX_LEVELS];    /* first index column bound at level L */
+    uint8_t lvl_ncol[SRDL_MAX_LEVELS];   /* columns bound at level L (0 = none) */
+} srdl_atom;
+
+/* One compiled rule instance (reference: planner.JoinPlan, planner.py:53-73). */
+typedef struct {
+    uint32_t depth;  /* number of variables m >= 1 */
+    uint32_t natoms;
+    uint32_t outer;  /* root source whose rows are flattened (Alg. 1)   */
+    uint32_t inner;  /* second root source or SRDL_NO_ATOM               */
+    uint32_t head_arity;
+    int32_t head_level[SRDL_MAX_HEAD];  /* >= 0: variable level; -1: constant */
+    uint32_t head_const[SRDL_MAX_HEAD];
+    uint32_t nspec[SRDL_MAX_LEVELS];    /* atoms with columns at level L       */
+    uint8_t spec[SRDL_MAX_LEVELS][SRDL_MAX_ATOMS];
+    uint8_t leaf_slot[SRDL_MAX_ATOMS];  /* position in spec[depth-1] or NO_ATOM */
+    srdl_atom atom[SRDL_MAX_ATOMS];
+} srdl_plan;
+
+/* at most this many atoms may constrain the last variable of a plan */
+#define SRDL_MAX_LEAF_SPECS 6
+
+/* Root work space of one plan execution (Alg. 1 phase 1, Fig. 2). */
+typedef struct {
+    const uint32_t *keys;    /* K root keys (outer histogram keys)            */
+    const uint32_t *d2;      /* K inner degrees (1 without inner source)      */
+    const uint64_t *prefix;  /* K inclusive prefix of outer_degree * d2       */
+    uint64_t nkeys;
+    uint32_t nwarps;         /* slices p; warp w owns [w*ceil(T/p), ...)      */
+    uint64_t *warp_counts;   /* p: tuples counted per slice                   */
+    uint64_t *warp_offsets;  /* p: exclusive prefix of warp_counts            */
+    uint64_t *total;         /* device scalar: sum of warp_counts             */
+    uint32_t *out[SRDL_MAX_HEAD];
+    uint32_t *error;         /* device flag, non-zero on count/write mismatch */
+    uint32_t *bitmap;        /* optional (audit): per-output-slot write counter */
+} srdl_exec;
+
+/* reference: executor.build_partition (executor.py:246). From the outer
+ * histogram (keys, degrees) and the inner histogram (may be empty), write
+ * d2[K] and the inclusive work prefix[K] (uint64). No host sync. */
+int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, uint64_t nk, const uint32_t *ikeys,
+                   const uint32_t *ideg, uint64_t nik, int has_inner, uint32_t *d2,
+                   uint64_t *prefix, void *stream);
+
+/* reference: executor.count_pass (executor.py:439). Count kernel over the
+ * flattened slices + exclusive scan into warp_offsets/total. No host sync. */
+int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream);
+
+/* reference: executor.materialize_pass (executor.py:458). Re-walks the
+ * slices writing head tuples at warp_offsets; sets *error on divergence. */
+int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stream);
+
+/* ------------------------------------------------------------- generators
+ * Synthetic inputs for the benchmarks (not on the evaluation path).
+ * R-MAT edge list (Chakrabarti et al.): n = 2^scale vertices, probabilities
+ * a, b, c (d = 1-a-b-c), counter-based RNG keyed by seed. */
+int srdl_gen_rmat(uint32_t scale, uint64_t nedges, float a, float b, float c, uint64_t seed,
+                  uint32_t *src, uint32_t *dst, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRDL_H */

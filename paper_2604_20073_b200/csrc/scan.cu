@@ -1,0 +1,203 @@
+// Device-wide scans (reduce-then-scan, warp-striped tiles), error plumbing,
+// stream-ordered scratch. Used by every counting / compaction step of the
+// two-phase pipeline (Alg. 1 "offsets <- PrefixSum(tc)").
+#include <stdarg.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace srdl {
+
+// ------------------------------------------------------------------ errors
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
+
+// ----------------------------------------------------------------- scratch
+
+static std::once_flag g_pool_once;
+
+static void tune_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t keep = ~0ull;  // never trim between iterations
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+}
+
+Scratch::Scratch(size_t bytes, cudaStream_t s) : stream_(s) {
+    std::call_once(g_pool_once, tune_pool);
+    if (bytes == 0) bytes = 16;
+    SRDL_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+}
+
+Scratch::~Scratch() {
+    if (ptr_) cudaFreeAsync(ptr_, stream_);
+}
+
+int sm_count() {
+    static int cached = 0;
+    if (!cached) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cached = n > 0 ? n : 148;
+    }
+    return cached;
+}
+
+uint64_t read_u64(const uint64_t *dev, cudaStream_t s) {
+    uint64_t v = 0;
+    SRDL_CUDA(cudaMemcpyAsync(&v, dev, sizeof(v), cudaMemcpyDeviceToHost, s));
+    SRDL_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+// ------------------------------------------------------------------- scans
+
+// Tile = 8 warps x 16 rounds x 32 lanes; element (w, r, l) is at
+// tile_base + w*512 + r*32 + l, so each warp owns a contiguous chunk and
+// every round is a coalesced 32-wide access.
+constexpr int kWarps = kThreads / 32;
+constexpr int kWarpChunk = 32 * kItems;
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) tile_reduce(const T *__restrict__ in, uint64_t n,
+                                                        T *__restrict__ partial) {
+    __shared__ T wsum[kWarps];
+    const uint64_t base = (uint64_t)blockIdx.x * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    T acc = 0;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
+        if (i < n) acc += in[i];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (l == 0) wsum[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T t = 0;
+        for (int k = 0; k < kWarps; ++k) t += wsum[k];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// Exclusive scan of one tile with an incoming block offset.
+template <class T, bool EXCLUSIVE>
+__global__ void __launch_bounds__(kThreads) tile_scan(const T *__restrict__ in, T *__restrict__ out,
+                                                      uint64_t n, const T *__restrict__ offsets,
+                                                      T *__restrict__ total) {
+    __shared__ T wsum[kWarps];
+    __shared__ T wbase[kWarps];
+    const uint64_t base = (uint64_t)blockIdx.x * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    T v[kItems];
+    T carry = 0;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
+        T x = i < n ? in[i] : T(0);
+        T s = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, s, o);
+            if (l >= o) s += y;
+        }
+        v[r] = carry + (EXCLUSIVE ? s - x : s);
+        carry += __shfl_sync(0xffffffffu, s, 31);
+    }
+    if (l == 0) wsum[w] = carry;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T run = offsets ? offsets[blockIdx.x] : T(0);
+        for (int k = 0; k < kWarps; ++k) {
+            wbase[k] = run;
+            run += wsum[k];
+        }
+        if (total && blockIdx.x == gridDim.x - 1) *total = run;
+    }
+    __syncthreads();
+    const T add = wbase[w];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
+        if (i < n) out[i] = v[r] + add;
+    }
+}
+
+template <class T>
+__global__ void write_zero(T *p) {
+    *p = 0;
+}
+
+template <class T, bool EXCLUSIVE>
+static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s) {
+    if (n == 0) {
+        if (total) {
+            write_zero<T><<<1, 1, 0, s>>>(total);
+            SRDL_CHECK_LAUNCH();
+        }
+        return;
+    }
+    const uint64_t blocks = (n + kTile - 1) / kTile;
+    if (blocks == 1) {
+        tile_scan<T, EXCLUSIVE><<<1, kThreads, 0, s>>>(in, out, n, nullptr, total);
+        SRDL_CHECK_LAUNCH();
+        return;
+    }
+    Scratch part(blocks * sizeof(T), s);
+    tile_reduce<T><<<(unsigned)blocks, kThreads, 0, s>>>(in, n, part.as<T>());
+    SRDL_CHECK_LAUNCH();
+    scan_impl<T, true>(part.as<T>(), part.as<T>(), blocks, nullptr, s);
+    tile_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, part.as<T>(), total);
+    SRDL_CHECK_LAUNCH();
+}
+
+void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *total,
+                        cudaStream_t s) {
+    scan_impl<uint64_t, true>(in, out, n, total, s);
+}
+void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *total,
+                        cudaStream_t s) {
+    scan_impl<uint32_t, true>(in, out, n, total, s);
+}
+void inclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, cudaStream_t s) {
+    scan_impl<uint64_t, false>(in, out, n, nullptr, s);
+}
+
+}  // namespace srdl
+
+extern "C" {
+
+int srdl_version(void) { return SRDL_VERSION; }
+
+uint64_t srdl_launch_count(void) { return srdl::launches(); }
+
+const char *srdl_last_error(void) { return srdl::g_err; }
+
+int srdl_sm_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        srdl::set_error("no CUDA device visible");
+        return SRDL_ERR_CUDA;
+    }
+    return srdl::sm_count();
+}
+
+}  // extern "C"

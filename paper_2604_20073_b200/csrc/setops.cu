@@ -1,0 +1,309 @@
+// Delta maintenance, part 2, and the root histogram pipeline:
+//  - rank merge of disjoint sorted row sets (head/body merge, Fig. 1 "Merge";
+//    reference ColumnarRelation.merge_delta, storage.py:272)
+//  - run-length histograms of a sorted key column and their incremental
+//    union (reference Histogram.over_column / updated, storage.py:48-76)
+//  - per-plan root work space: d2 lookup + prefix of outer_deg * d2
+//    (reference executor.build_partition, executor.py:246-274; paper Alg. 1)
+//  - constant-prefix narrowing (reference executor.prepare, executor.py:188)
+//  - the synthetic R-MAT generator used by the benchmarks.
+#include "common.cuh"
+
+namespace srdl {
+
+// out[i + |{b < a_i}|] = a_i ; out[j + |{a < b_j}|] = b_j  (disjoint inputs)
+__global__ void rank_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity,
+                                MutCols out) {
+    const uint64_t n = na + nb;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t dst;
+        const Cols *src;
+        uint64_t row;
+        if (t < na) {
+            row = t;
+            src = &A;
+            dst = t + row_bound(B, 0, nb, A, row, arity, false);
+        } else {
+            row = t - na;
+            src = &B;
+            dst = row + row_bound(A, 0, na, B, row, arity, false);
+        }
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][dst] = __ldg(src->c[c] + row);
+    }
+}
+
+__global__ void run_flags(const uint32_t *__restrict__ col, uint64_t n, uint32_t *__restrict__ f) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        f[i] = (i == 0) || col[i] != col[i - 1];
+}
+
+__global__ void run_starts(const uint32_t *__restrict__ col, const uint32_t *__restrict__ f,
+                           const uint32_t *__restrict__ pos, uint64_t n, uint32_t *__restrict__ keys,
+                           uint32_t *__restrict__ starts) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (f[i]) {
+            keys[pos[i]] = col[i];
+            starts[pos[i]] = (uint32_t)i;
+        }
+    }
+}
+
+__global__ void run_lengths(const uint32_t *__restrict__ starts, const uint32_t *__restrict__ kdev,
+                            uint64_t n, uint32_t *__restrict__ deg, uint64_t *__restrict__ deg64) {
+    const uint64_t K = *kdev;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < K;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t end = k + 1 < K ? starts[k + 1] : n;
+        uint32_t d = (uint32_t)(end - starts[k]);
+        deg[k] = d;
+        deg64[k] = d;
+    }
+}
+
+// merged (key, degree) lists with ties kept adjacent (A before B)
+__global__ void rank_merge_hist(const uint32_t *__restrict__ ka, const uint32_t *__restrict__ da,
+                                uint64_t na, const uint32_t *__restrict__ kb,
+                                const uint32_t *__restrict__ db, uint64_t nb,
+                                uint32_t *__restrict__ mk, uint32_t *__restrict__ md) {
+    const uint64_t n = na + nb;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        if (t < na) {
+            uint32_t k = ka[t];
+            uint64_t lo = 0, hi = nb;
+            while (lo < hi) {
+                uint64_t m = (lo + hi) >> 1;
+                if (kb[m] < k) lo = m + 1; else hi = m;
+            }
+            mk[t + lo] = k;
+            md[t + lo] = da[t];
+        } else {
+            uint64_t j = t - na;
+            uint32_t k = kb[j];
+            uint64_t lo = 0, hi = na;
+            while (lo < hi) {
+                uint64_t m = (lo + hi) >> 1;
+                if (ka[m] <= k) lo = m + 1; else hi = m;
+            }
+            mk[j + lo] = k;
+            md[j + lo] = db[j];
+        }
+    }
+}
+
+__global__ void combine_pairs(const uint32_t *__restrict__ mk, const uint32_t *__restrict__ md,
+                              const uint32_t *__restrict__ f, const uint32_t *__restrict__ pos,
+                              uint64_t n, uint32_t *__restrict__ keys, uint32_t *__restrict__ deg,
+                              uint64_t *__restrict__ deg64) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!f[i]) continue;
+        uint32_t d = md[i];
+        if (i + 1 < n && mk[i + 1] == mk[i]) d += md[i + 1];
+        keys[pos[i]] = mk[i];
+        deg[pos[i]] = d;
+        deg64[pos[i]] = d;
+    }
+}
+
+__global__ void root_work_kernel(const uint32_t *__restrict__ okeys, const uint32_t *__restrict__ odeg,
+                                 uint64_t nk, const uint32_t *__restrict__ ikeys,
+                                 const uint32_t *__restrict__ ideg, uint64_t nik, int has_inner,
+                                 uint32_t *__restrict__ d2, uint64_t *__restrict__ work) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t d = 1;
+        if (has_inner) {
+            uint32_t k = okeys[i];
+            uint64_t lo = 0, hi = nik;
+            while (lo < hi) {
+                uint64_t m = (lo + hi) >> 1;
+                if (ikeys[m] < k) lo = m + 1; else hi = m;
+            }
+            d = (lo < nik && ikeys[lo] == k) ? ideg[lo] : 0u;
+        }
+        d2[i] = d;
+        work[i] = (uint64_t)odeg[i] * d;
+    }
+}
+
+__global__ void narrow_prefix_kernel(Cols cols, uint64_t n, const uint32_t *__restrict__ vals,
+                                     uint32_t nv, uint64_t *__restrict__ range) {
+    uint64_t lo = 0, hi = n;
+    for (uint32_t c = 0; c < nv && lo < hi; ++c) {
+        const uint32_t *col = cols.c[c];
+        uint32_t v = vals[c];
+        uint64_t a = lo, b = hi;
+        while (a < b) {
+            uint64_t m = (a + b) >> 1;
+            if (col[m] < v) a = m + 1; else b = m;
+        }
+        uint64_t e = a, f = hi;
+        while (e < f) {
+            uint64_t m = (e + f) >> 1;
+            if (col[m] <= v) e = m + 1; else f = m;
+        }
+        lo = a;
+        hi = e;
+    }
+    if (lo > hi) hi = lo;
+    range[0] = lo;
+    range[1] = hi;
+}
+
+// counter-based RNG: splitmix64 finaliser over (seed, edge, level)
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+__global__ void rmat_kernel(uint32_t scale, uint64_t m, float a, float b, float c, uint64_t seed,
+                            uint32_t *__restrict__ src, uint32_t *__restrict__ dst) {
+    const float ab = a + b, abc = a + b + c;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t u = 0, v = 0;
+        uint64_t state = mix64(seed * 0x9e3779b97f4a7c15ull + e);
+        for (uint32_t lvl = 0; lvl < scale; ++lvl) {
+            state = mix64(state + 0x9e3779b97f4a7c15ull);
+            float r = (float)(state >> 40) * (1.0f / 16777216.0f);
+            uint32_t sb = r >= ab;
+            uint32_t db = (r >= a && r < ab) || r >= abc;
+            u |= sb << lvl;
+            v |= db << lvl;
+        }
+        src[e] = u;
+        dst[e] = v;
+    }
+}
+
+static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *degrees,
+                               uint64_t *prefix, cudaStream_t s) {
+    if (n == 0) return 0;
+    SRDL_REQUIRE(n < (1ull << 32), "histogram: column longer than 2^32");
+    const unsigned g = stride_grid(n);
+    Scratch f(n * sizeof(uint32_t), s), pos(n * sizeof(uint32_t), s), starts(n * sizeof(uint32_t), s);
+    Scratch k(sizeof(uint32_t) * 2, s), deg64(n * sizeof(uint64_t), s);
+    run_flags<<<g, kThreads, 0, s>>>(col, n, f.as<uint32_t>());
+    SRDL_CHECK_LAUNCH();
+    exclusive_scan_u32(f.as<uint32_t>(), pos.as<uint32_t>(), n, k.as<uint32_t>(), s);
+    run_starts<<<g, kThreads, 0, s>>>(col, f.as<uint32_t>(), pos.as<uint32_t>(), n, keys,
+                                      starts.as<uint32_t>());
+    SRDL_CHECK_LAUNCH();
+    run_lengths<<<g, kThreads, 0, s>>>(starts.as<uint32_t>(), k.as<uint32_t>(), n, degrees,
+                                       deg64.as<uint64_t>());
+    SRDL_CHECK_LAUNCH();
+    uint32_t K = 0;
+    SRDL_CUDA(cudaMemcpyAsync(&K, k.as<uint32_t>(), sizeof(K), cudaMemcpyDeviceToHost, s));
+    SRDL_CUDA(cudaStreamSynchronize(s));
+    inclusive_scan_u64(deg64.as<uint64_t>(), prefix, K, s);
+    return K;
+}
+
+}  // namespace srdl
+
+using namespace srdl;
+
+extern "C" {
+
+int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, uint64_t nb,
+               uint32_t arity, uint32_t *const *out, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(arity >= 1 && arity <= SRDL_MAX_COLS, "arity %u out of range", arity);
+        const uint64_t n = na + nb;
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        Cols A = na ? make_cols(a, arity) : Cols{};
+        Cols B = nb ? make_cols(b, arity) : Cols{};
+        rank_merge_rows<<<stride_grid(n), kThreads, 0, s>>>(A, na, B, nb, arity,
+                                                            make_mut(out, arity));
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+int srdl_histogram(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *degrees,
+                   uint64_t *prefix, uint64_t *k_out, void *stream) {
+    return guarded([&] { *k_out = histogram_impl(col, n, keys, degrees, prefix, (cudaStream_t)stream); });
+}
+
+int srdl_histogram_merge(const uint32_t *ka, const uint32_t *da, uint64_t na, const uint32_t *kb,
+                         const uint32_t *db, uint64_t nb, uint32_t *keys, uint32_t *degrees,
+                         uint64_t *prefix, uint64_t *k_out, void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        const uint64_t n = na + nb;
+        *k_out = 0;
+        if (n == 0) return;
+        const unsigned g = stride_grid(n);
+        Scratch mk(n * sizeof(uint32_t), s), md(n * sizeof(uint32_t), s);
+        Scratch f(n * sizeof(uint32_t), s), pos(n * sizeof(uint32_t), s);
+        Scratch k(sizeof(uint32_t) * 2, s), deg64(n * sizeof(uint64_t), s);
+        rank_merge_hist<<<g, kThreads, 0, s>>>(ka, da, na, kb, db, nb, mk.as<uint32_t>(),
+                                               md.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        run_flags<<<g, kThreads, 0, s>>>(mk.as<uint32_t>(), n, f.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u32(f.as<uint32_t>(), pos.as<uint32_t>(), n, k.as<uint32_t>(), s);
+        combine_pairs<<<g, kThreads, 0, s>>>(mk.as<uint32_t>(), md.as<uint32_t>(), f.as<uint32_t>(),
+                                             pos.as<uint32_t>(), n, keys, degrees,
+                                             deg64.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        uint32_t K = 0;
+        SRDL_CUDA(cudaMemcpyAsync(&K, k.as<uint32_t>(), sizeof(K), cudaMemcpyDeviceToHost, s));
+        SRDL_CUDA(cudaStreamSynchronize(s));
+        inclusive_scan_u64(deg64.as<uint64_t>(), prefix, K, s);
+        *k_out = K;
+    });
+}
+
+int srdl_narrow_prefix(const uint32_t *const *cols, uint64_t n, const uint32_t *values,
+                       uint32_t nvalues, uint64_t *lo, uint64_t *hi, void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        SRDL_REQUIRE(nvalues <= SRDL_MAX_COLS, "too many constant columns");
+        Scratch dv(sizeof(uint32_t) * SRDL_MAX_COLS + 2 * sizeof(uint64_t), s);
+        uint32_t *vals = dv.as<uint32_t>();
+        uint64_t *range = reinterpret_cast<uint64_t *>(vals + SRDL_MAX_COLS);
+        SRDL_CUDA(cudaMemcpyAsync(vals, values, nvalues * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        narrow_prefix_kernel<<<1, 1, 0, s>>>(make_cols(cols, nvalues), n, vals, nvalues, range);
+        SRDL_CHECK_LAUNCH();
+        uint64_t h[2];
+        SRDL_CUDA(cudaMemcpyAsync(h, range, sizeof(h), cudaMemcpyDeviceToHost, s));
+        SRDL_CUDA(cudaStreamSynchronize(s));
+        *lo = h[0];
+        *hi = h[1];
+    });
+}
+
+int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, uint64_t nk, const uint32_t *ikeys,
+                   const uint32_t *ideg, uint64_t nik, int has_inner, uint32_t *d2,
+                   uint64_t *prefix, void *stream) {
+    return guarded([&] {
+        if (nk == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        root_work_kernel<<<stride_grid(nk), kThreads, 0, s>>>(okeys, odeg, nk, ikeys, ideg, nik,
+                                                              has_inner, d2, prefix);
+        SRDL_CHECK_LAUNCH();
+        inclusive_scan_u64(prefix, prefix, nk, s);
+    });
+}
+
+int srdl_gen_rmat(uint32_t scale, uint64_t nedges, float a, float b, float c, uint64_t seed,
+                  uint32_t *src, uint32_t *dst, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(scale >= 1 && scale <= 32, "scale %u outside [1, 32]", scale);
+        if (nedges == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        rmat_kernel<<<stride_grid(nedges), kThreads, 0, s>>>(scale, nedges, a, b, c, seed, src, dst);
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,384 @@
+// Delta maintenance, part 1: LSD radix sort of packed tuples, unique, and the
+// anti-join against the full relation (paper Fig. 1 "Compute Delta" /
+// "Build Index"; reference storage.compute_delta, storage.py:311, and
+// rowops.sort_dedup, rowops.py:60).
+//
+// Tuples of `arity` u32 ids with `bits` significant bits each are packed
+// into u64 keys, column 0 most significant, so the numeric order of keys is
+// the lexicographic order of rows. When arity*bits > 64 the columns are
+// split into chunks of at most 64 bits, sorted least-significant chunk first
+// with a stable radix sort carrying a row permutation.
+#include "common.cuh"
+
+namespace srdl {
+
+constexpr int kRadixBits = 8;
+constexpr int kBins = 1 << kRadixBits;
+constexpr int kWarps = kThreads / 32;
+constexpr int kWarpChunk = 32 * kItems;
+
+__device__ __forceinline__ uint64_t tile_index(int w, int r, int l) {
+    return (uint64_t)blockIdx.x * kTile + (uint64_t)w * kWarpChunk + r * 32 + l;
+}
+
+// Per-block digit histogram, written digit-major: counts[d * nblocks + b].
+__global__ void __launch_bounds__(kThreads)
+    radix_hist(const uint64_t *__restrict__ keys, uint64_t n, int shift, uint32_t *counts) {
+    __shared__ uint32_t h[kWarps][kBins];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = tile_index(w, r, l);
+        if (i < n) atomicAdd(&h[w][(keys[i] >> shift) & (kBins - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kBins; d += kThreads) {
+        uint32_t t = 0;
+#pragma unroll
+        for (int k = 0; k < kWarps; ++k) t += h[k][d];
+        counts[(uint64_t)d * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// Stable scatter: rank within the tile via warp match + per-warp counters.
+template <bool HAS_VALS>
+__global__ void __launch_bounds__(kThreads)
+    radix_scatter(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n,
+                  int shift, const uint32_t *__restrict__ offsets, uint64_t *__restrict__ keys_out,
+                  uint32_t *__restrict__ vals_out) {
+    __shared__ uint32_t cnt[kWarps][kBins];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    uint64_t k[kItems];
+    uint32_t v[kItems];
+    uint32_t rank[kItems];
+    const uint32_t lt = (1u << l) - 1u;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = tile_index(w, r, l);
+        bool ok = i < n;
+        k[r] = ok ? keys[i] : 0;
+        if (HAS_VALS) v[r] = ok ? vals[i] : 0;
+        uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t before = 0;
+        if (ok) before = cnt[w][d];
+        __syncwarp();
+        if (ok && (peers & lt) == 0) cnt[w][d] = before + __popc(peers);
+        __syncwarp();
+        rank[r] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kBins; d += kThreads) {
+        uint32_t run = offsets[(uint64_t)d * gridDim.x + blockIdx.x];
+#pragma unroll
+        for (int q = 0; q < kWarps; ++q) {
+            uint32_t c = cnt[q][d];
+            cnt[q][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        uint64_t i = tile_index(w, r, l);
+        if (i < n) {
+            uint32_t d = (uint32_t)((k[r] >> shift) & (kBins - 1));
+            uint32_t pos = cnt[w][d] + rank[r];
+            keys_out[pos] = k[r];
+            if (HAS_VALS) vals_out[pos] = v[r];
+        }
+    }
+}
+
+void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s) {
+    if (n <= 1 || bits == 0) return;
+    SRDL_REQUIRE(n < (1ull << 32), "radix_sort: %llu rows exceeds the 32-bit rank space",
+                 (unsigned long long)n);
+    const uint64_t blocks = (n + kTile - 1) / kTile;
+    const int passes = (int)((bits + kRadixBits - 1) / kRadixBits);
+    Scratch kalt(n * sizeof(uint64_t), s);
+    Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);
+    Scratch counts(blocks * kBins * sizeof(uint32_t), s);
+    uint64_t *kin = keys, *kout = kalt.as<uint64_t>();
+    uint32_t *vin = vals, *vout = vals ? valt.as<uint32_t>() : nullptr;
+    for (int p = 0; p < passes; ++p) {
+        int shift = p * kRadixBits;
+        radix_hist<<<(unsigned)blocks, kThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u32(counts.as<uint32_t>(), counts.as<uint32_t>(), blocks * kBins, nullptr, s);
+        if (vals)
+            radix_scatter<true><<<(unsigned)blocks, kThreads, 0, s>>>(
+                kin, vin, n, shift, counts.as<uint32_t>(), kout, vout);
+        else
+            radix_scatter<false><<<(unsigned)blocks, kThreads, 0, s>>>(
+                kin, nullptr, n, shift, counts.as<uint32_t>(), kout, nullptr);
+        SRDL_CHECK_LAUNCH();
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    if (kin != keys) {
+        SRDL_CUDA(cudaMemcpyAsync(keys, kin, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        if (vals)
+            SRDL_CUDA(cudaMemcpyAsync(vals, vin, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    }
+}
+
+// ----------------------------------------------------------- pack / unpack
+
+struct Chunk {
+    uint32_t first, count;  // columns [first, first+count)
+};
+
+__global__ void pack_keys(Cols cols, Chunk ch, uint32_t bits, const uint32_t *__restrict__ perm,
+                          uint64_t n, uint64_t *__restrict__ keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t row = perm ? perm[i] : i;
+        uint64_t k = 0;
+        for (uint32_t c = 0; c < ch.count; ++c) k = (k << bits) | __ldg(cols.c[ch.first + c] + row);
+        keys[i] = k;
+    }
+}
+
+__global__ void iota_u32(uint32_t *p, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)i;
+}
+
+// pack row j of a sorted segment with the same layout as the staged keys
+__device__ __forceinline__ uint64_t pack_row(const Cols &c, uint64_t j, uint32_t arity,
+                                             uint32_t bits) {
+    uint64_t k = 0;
+    for (uint32_t q = 0; q < arity; ++q) k = (k << bits) | __ldg(c.c[q] + j);
+    return k;
+}
+
+struct Segs {
+    Cols seg[SRDL_MAX_SEGS];
+    uint64_t rows[SRDL_MAX_SEGS];
+    uint32_t nseg;
+};
+
+__device__ __forceinline__ bool segs_contain_key(const Segs &S, uint64_t key, uint32_t arity,
+                                                 uint32_t bits) {
+    for (uint32_t s = 0; s < S.nseg; ++s) {
+        uint64_t lo = 0, hi = S.rows[s];
+        while (lo < hi) {
+            uint64_t mid = lo + ((hi - lo) >> 1);
+            if (pack_row(S.seg[s], mid, arity, bits) < key)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        if (lo < S.rows[s] && pack_row(S.seg[s], lo, arity, bits) == key) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool segs_contain_row(const Segs &S, const Cols &A, uint64_t i,
+                                                 uint32_t arity) {
+    for (uint32_t s = 0; s < S.nseg; ++s) {
+        uint64_t pos = row_bound(S.seg[s], 0, S.rows[s], A, i, arity, false);
+        if (pos < S.rows[s] && row_cmp(S.seg[s], pos, A, i, arity) == 0) return true;
+    }
+    return false;
+}
+
+// keep[i] = first of its run of equal keys and absent from the full segments
+__global__ void flag_keys(const uint64_t *__restrict__ keys, uint64_t n, Segs S, uint32_t arity,
+                          uint32_t bits, uint32_t *__restrict__ keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        bool f = (i == 0) || keys[i - 1] != k;
+        if (f && S.nseg) f = !segs_contain_key(S, k, arity, bits);
+        keep[i] = f;
+    }
+}
+
+__global__ void scatter_unpack(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ keep,
+                               const uint32_t *__restrict__ pos, uint64_t n, uint32_t arity,
+                               uint32_t bits, MutCols out) {
+    const uint64_t mask = bits >= 32 ? 0xffffffffull : ((1ull << bits) - 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!keep[i]) continue;
+        uint64_t k = keys[i];
+        uint32_t p = pos[i];
+        for (int c = (int)arity - 1; c >= 0; --c) {
+            out.c[c][p] = (uint32_t)(k & mask);
+            k >>= bits;
+        }
+    }
+}
+
+// general path (arity*bits > 64): rows already gathered into sorted order
+__global__ void flag_rows(Cols rows, uint64_t n, Segs S, uint32_t arity, uint32_t *__restrict__ keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        bool f = (i == 0) || row_cmp(rows, i - 1, rows, i, arity) != 0;
+        if (f && S.nseg) f = !segs_contain_row(S, rows, i, arity);
+        keep[i] = f;
+    }
+}
+
+__global__ void scatter_rows(Cols rows, const uint32_t *__restrict__ keep,
+                             const uint32_t *__restrict__ pos, uint64_t n, uint32_t arity,
+                             MutCols out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!keep[i]) continue;
+        uint32_t p = pos[i];
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][p] = __ldg(rows.c[c] + i);
+    }
+}
+
+__global__ void gather_cols(Cols cols, uint32_t arity, const uint32_t *__restrict__ idx, uint64_t n,
+                            MutCols out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t r = idx[i];
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][i] = __ldg(cols.c[c] + r);
+    }
+}
+
+__global__ void check_sorted(Cols rows, uint64_t n, uint32_t arity, int *bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (row_cmp(rows, i, rows, i + 1, arity) >= 0) atomicExch(bad, 1);
+    }
+}
+
+// Sort + unique + anti-join; the heart of compute_delta.
+static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, uint64_t n,
+                                  uint32_t bits, const Segs &S, uint32_t *const *out,
+                                  cudaStream_t s) {
+    SRDL_REQUIRE(arity >= 1 && arity <= SRDL_MAX_COLS, "arity %u outside [1, %d]", arity,
+                 SRDL_MAX_COLS);
+    SRDL_REQUIRE(bits >= 1 && bits <= 32, "bits %u outside [1, 32]", bits);
+    if (n == 0) return 0;
+    SRDL_REQUIRE(n < (1ull << 32), "sort: %llu rows exceeds 2^32", (unsigned long long)n);
+    Cols in = make_cols(cols, arity);
+    MutCols dst = make_mut(out, arity);
+    const unsigned g = stride_grid(n);
+    Scratch keys(n * sizeof(uint64_t), s);
+    Scratch keep(n * sizeof(uint32_t), s);
+    Scratch total(sizeof(uint32_t) * 2, s);
+    const uint32_t per_chunk = 64 / bits;
+    if (arity <= per_chunk) {
+        pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, arity}, bits, nullptr, n, keys.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        radix_sort(keys.as<uint64_t>(), nullptr, n, arity * bits, s);
+        flag_keys<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), n, S, arity, bits, keep.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        Scratch pos(n * sizeof(uint32_t), s);
+        exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
+        scatter_unpack<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), keep.as<uint32_t>(),
+                                              pos.as<uint32_t>(), n, arity, bits, dst);
+        SRDL_CHECK_LAUNCH();
+    } else {
+        Scratch perm(n * sizeof(uint32_t), s);
+        iota_u32<<<g, kThreads, 0, s>>>(perm.as<uint32_t>(), n);
+        SRDL_CHECK_LAUNCH();
+        // least significant chunk first; chunks end at the last column
+        int end = (int)arity;
+        while (end > 0) {
+            int first = end - (int)per_chunk;
+            if (first < 0) first = 0;
+            Chunk ch{(uint32_t)first, (uint32_t)(end - first)};
+            pack_keys<<<g, kThreads, 0, s>>>(in, ch, bits, perm.as<uint32_t>(), n,
+                                             keys.as<uint64_t>());
+            SRDL_CHECK_LAUNCH();
+            radix_sort(keys.as<uint64_t>(), perm.as<uint32_t>(), n, ch.count * bits, s);
+            end = first;
+        }
+        Scratch sorted(n * sizeof(uint32_t) * arity, s);
+        MutCols tmp{};
+        Cols tmpc{};
+        for (uint32_t c = 0; c < arity; ++c) {
+            tmp.c[c] = sorted.as<uint32_t>() + c * n;
+            tmpc.c[c] = tmp.c[c];
+        }
+        gather_cols<<<g, kThreads, 0, s>>>(in, arity, perm.as<uint32_t>(), n, tmp);
+        SRDL_CHECK_LAUNCH();
+        flag_rows<<<g, kThreads, 0, s>>>(tmpc, n, S, arity, keep.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        Scratch pos(n * sizeof(uint32_t), s);
+        exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
+        scatter_rows<<<g, kThreads, 0, s>>>(tmpc, keep.as<uint32_t>(), pos.as<uint32_t>(), n, arity,
+                                            dst);
+        SRDL_CHECK_LAUNCH();
+    }
+    uint32_t cnt = 0;
+    SRDL_CUDA(cudaMemcpyAsync(&cnt, total.as<uint32_t>(), sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    SRDL_CUDA(cudaStreamSynchronize(s));
+    return cnt;
+}
+
+}  // namespace srdl
+
+using namespace srdl;
+
+extern "C" {
+
+int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                    uint32_t *const *out, uint64_t *n_out, void *stream) {
+    return guarded([&] {
+        Segs none{};
+        none.nseg = 0;
+        *n_out = sort_unique_minus(cols, arity, n, bits, none, out, (cudaStream_t)stream);
+    });
+}
+
+int srdl_compute_delta(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                       const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,
+                       uint32_t nseg, uint32_t *const *out, uint64_t *n_out, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(nseg <= SRDL_MAX_SEGS, "at most %d full segments", SRDL_MAX_SEGS);
+        Segs S{};
+        S.nseg = 0;
+        for (uint32_t q = 0; q < nseg; ++q) {
+            if (seg_rows[q] == 0) continue;
+            S.seg[S.nseg] = make_cols(seg_cols[q], arity);
+            S.rows[S.nseg] = seg_rows[q];
+            S.nseg++;
+        }
+        *n_out = sort_unique_minus(cols, arity, n, bits, S, out, (cudaStream_t)stream);
+    });
+}
+
+int srdl_is_sorted_strict(const uint32_t *const *cols, uint32_t arity, uint64_t n, int *ok,
+                          void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        *ok = 1;
+        if (n <= 1) return;
+        Scratch bad(sizeof(int), s);
+        SRDL_CUDA(cudaMemsetAsync(bad.as<int>(), 0, sizeof(int), s));
+        check_sorted<<<stride_grid(n), kThreads, 0, s>>>(make_cols(cols, arity), n, arity,
+                                                        bad.as<int>());
+        SRDL_CHECK_LAUNCH();
+        int h = 0;
+        SRDL_CUDA(cudaMemcpyAsync(&h, bad.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        SRDL_CUDA(cudaStreamSynchronize(s));
+        *ok = !h;
+    });
+}
+
+int srdl_gather(const uint32_t *const *cols, uint32_t arity, const uint32_t *idx, uint64_t n,
+                uint32_t *const *out, void *stream) {
+    return guarded([&] {
+        if (n == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        gather_cols<<<stride_grid(n), kThreads, 0, s>>>(make_cols(cols, arity), arity, idx, n,
+                                                        make_mut(out, arity));
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,503 @@
+// Histogram-guided, warp-cooperative worst-case-optimal join (paper Alg. 1
+// phases 2-3 and Alg. 2; reference executor.count_pass / materialize_pass /
+// _run_slice / _root_setup / _descend, executor.py:342-485).
+//
+// Work decomposition. The root level is flattened into T = sum_k outer(k) *
+// d2(k) units (prefix array C). Warp w owns units [w*ceil(T/p), (w+1)*ceil(T/p)),
+// finds its first key by binary search on C (kappa) and walks its slice as
+// at most three (outer rows x inner rows) rectangles per key, exactly the
+// Fig. 2 scheme, so a heavy root key is spread over many warps.
+//
+// Inside a rectangle the warp runs leapfrog-style generic join over the
+// remaining levels with all 32 lanes cooperating:
+//   * candidates of a level come 32 at a time from the source with the
+//     smallest narrowed range (run starts = distinct values), every lane
+//     narrows the other sources for its own candidate by binary search, and
+//     a ballot keeps the survivors (no atomics anywhere);
+//   * levels 1..m-3 descend survivor by survivor (DFS state in shared memory);
+//   * the last two levels are flattened: the survivors of level m-2 become a
+//     batch of up to 32 parents, their leaf candidate ranges are prefix-summed
+//     across the warp and all lanes walk the concatenated ranges, so a leaf
+//     with short fan-out still keeps the warp full and output writes stay
+//     coalesced (the paper's "adjacent threads emit adjacent positions").
+// Count and materialize run the same code (template flag WRITE), so per-warp
+// counts are exact and writes land in [offset_w, offset_w + count_w).
+#include "common.cuh"
+
+namespace srdl {
+
+constexpr int kJoinWarps = 4;
+constexpr uint32_t kFull = 0xffffffffu;
+
+struct Rng {
+    uint32_t lo, hi;
+};
+
+struct WarpState {
+    uint32_t bind[SRDL_MAX_LEVELS];
+    Rng rng[SRDL_MAX_LEVELS + 1][SRDL_MAX_ATOMS][SRDL_MAX_SEGS];  // ranges on entry of level L
+    uint32_t vals[SRDL_MAX_LEVELS][32];                           // candidates of current chunk
+    uint32_t cur[SRDL_MAX_LEVELS];                                // next driver row
+    uint32_t mask[SRDL_MAX_LEVELS];                               // survivors not yet descended
+    uint8_t drv[SRDL_MAX_LEVELS];
+    uint8_t dseg[SRDL_MAX_LEVELS];
+    Rng leaf[32][SRDL_MAX_LEAF_SPECS][SRDL_MAX_SEGS];            // per-parent leaf ranges
+    uint64_t leaf_pref[33];
+    uint8_t leaf_drv[32];
+};
+
+__device__ __forceinline__ uint32_t lbound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
+                                           uint32_t v) {
+    while (lo < hi) {
+        uint32_t mid = lo + ((hi - lo) >> 1);
+        if (__ldg(col + mid) < v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
+                                           uint32_t v) {
+    while (lo < hi) {
+        uint32_t mid = lo + ((hi - lo) >> 1);
+        if (__ldg(col + mid) <= v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Narrow r (rows of segment s of atom A) to rows whose level-L columns all
+// equal v. Returns the new length (0 = no match).
+__device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
+    const int c0 = A.lvl_col[L], nc = A.lvl_ncol[L];
+    uint32_t lo = r.lo, hi = r.hi;
+    for (int c = c0; c < c0 + nc && lo < hi; ++c) {
+        const uint32_t *col = A.seg[s].cols[c];
+        uint32_t a = lbound(col, lo, hi, v);
+        hi = ubound(col, a, hi, v);
+        lo = a;
+    }
+    if (lo >= hi) hi = lo;
+    r.lo = lo;
+    r.hi = hi;
+    return hi - lo;
+}
+
+__device__ __forceinline__ uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
+    const uint32_t *col = A.seg[s].cols[A.lvl_col[L]];
+    uint32_t a = lbound(col, r.lo, r.hi, v);
+    uint32_t b = ubound(col, a, r.hi, v);
+    r.lo = a;
+    r.hi = b;
+    return b - a;
+}
+
+template <bool WRITE>
+struct Sink {
+    uint64_t n;       // tuples emitted so far by this warp (uniform)
+    uint64_t base;    // write offset of this warp (materialize)
+    __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const WarpState &S,
+                                         bool alive, uint32_t parent, uint32_t v, int leaf) {
+        const uint32_t m = __ballot_sync(kFull, alive);
+        if (WRITE && alive) {
+            const uint64_t pos = base + n + __popc(m & ((1u << lane_id()) - 1u));
+            for (uint32_t h = 0; h < P.head_arity; ++h) {
+                const int lvl = P.head_level[h];
+                uint32_t val;
+                if (lvl < 0)
+                    val = P.head_const[h];
+                else if (lvl == leaf)
+                    val = v;
+                else if (lvl == leaf - 1)
+                    val = S.vals[leaf - 1][parent];
+                else
+                    val = S.bind[lvl];
+                X.out[h][pos] = val;
+            }
+            if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
+        }
+        n += __popc(m);
+    }
+};
+
+// Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
+// level m-2 chunk; for m == 2 the single parent is the root rectangle).
+template <bool WRITE>
+__device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t parents,
+                           Sink<WRITE> &sink) {
+    const int leaf = (int)P.depth - 1;
+    const uint32_t nls = P.nspec[leaf];
+    const uint32_t l = lane_id();
+    uint64_t len = 0;
+    if ((parents >> l) & 1u) {
+        uint32_t best = 0xffffffffu, bj = 0;
+        for (uint32_t j = 0; j < nls; ++j) {
+            const srdl_atom &A = P.atom[P.spec[leaf][j]];
+            if (A.negated) continue;
+            uint32_t t = 0;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.leaf[l][j][s].hi - S.leaf[l][j][s].lo;
+            if (t < best) {
+                best = t;
+                bj = j;
+            }
+        }
+        len = best;
+        S.leaf_drv[l] = (uint8_t)bj;
+    }
+    uint64_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(kFull, incl, o);
+        if (l >= (uint32_t)o) incl += y;
+    }
+    S.leaf_pref[l] = incl - len;
+    const uint64_t total = __shfl_sync(kFull, incl, 31);
+    if (l == 31) S.leaf_pref[32] = total;
+    __syncwarp();
+    for (uint64_t base = 0; base < total; base += 32) {
+        const uint64_t f = base + l;
+        bool alive = f < total;
+        uint32_t p = 0, v = 0;
+        if (alive) {
+            // owner: last p with pref[p] <= f
+            uint32_t lo = 0, hi = 32;
+            while (lo < hi) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (S.leaf_pref[mid] <= f)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            p = lo - 1;
+            const uint32_t j = S.leaf_drv[p];
+            const uint32_t da = P.spec[leaf][j];
+            const srdl_atom &D = P.atom[da];
+            uint64_t local = f - S.leaf_pref[p];
+            const Rng r0 = S.leaf[p][j][0];
+            const uint32_t n0 = r0.hi - r0.lo;
+            int s = 0;
+            uint32_t row, seg_lo;
+            if (local < n0) {
+                row = r0.lo + (uint32_t)local;
+                seg_lo = r0.lo;
+            } else {
+                s = 1;
+                seg_lo = S.leaf[p][j][1].lo;
+                row = seg_lo + (uint32_t)(local - n0);
+            }
+            const uint32_t *col = D.seg[s].cols[D.lvl_col[leaf]];
+            v = __ldg(col + row);
+            alive = row == seg_lo || __ldg(col + row - 1) != v;
+            if (alive && s == 1 && n0) {
+                Rng t = r0;
+                alive = narrow_first(D, 0, leaf, v, t) == 0;  // already produced by segment 0
+            }
+            for (uint32_t jj = 0; jj < nls && alive; ++jj) {
+                const srdl_atom &A = P.atom[P.spec[leaf][jj]];
+                if (jj == j && A.lvl_ncol[leaf] == 1) continue;
+                uint32_t tot = 0;
+                for (uint32_t q = 0; q < A.nseg; ++q) {
+                    Rng t = S.leaf[p][jj][q];
+                    if (t.lo < t.hi) tot += narrow(A, q, leaf, v, t);
+                }
+                if (A.negated ? tot != 0 : tot == 0) alive = false;
+            }
+        }
+        sink.emit(P, X, S, alive, p, v, leaf);
+    }
+    __syncwarp();
+}
+
+// Pick the smallest candidate source of level L and reset the chunk cursor.
+__device__ __forceinline__ void open_level(const srdl_plan &P, WarpState &S, int L) {
+    if (lane_id() == 0) {
+        uint32_t best = 0xffffffffu, ba = 0;
+        for (uint32_t j = 0; j < P.nspec[L]; ++j) {
+            const uint32_t a = P.spec[L][j];
+            const srdl_atom &A = P.atom[a];
+            if (A.negated) continue;
+            uint32_t t = 0;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.rng[L][a][s].hi - S.rng[L][a][s].lo;
+            if (t < best) {
+                best = t;
+                ba = a;
+            }
+        }
+        S.drv[L] = (uint8_t)ba;
+        S.dseg[L] = 0;
+        S.cur[L] = S.rng[L][ba][0].lo;
+        S.mask[L] = 0;
+    }
+    __syncwarp();
+}
+
+// Next 32 driver rows of level L -> filtered candidates. False when exhausted.
+template <bool WRITE>
+__device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, WarpState &S, int L,
+                           Sink<WRITE> &sink) {
+    const uint32_t l = lane_id();
+    const uint32_t a = S.drv[L];
+    const srdl_atom &D = P.atom[a];
+    uint32_t s = S.dseg[L];
+    uint32_t r = S.cur[L];
+    while (true) {
+        if (s >= D.nseg) return false;
+        if (r < S.rng[L][a][s].hi) break;
+        ++s;
+        if (s < D.nseg) r = S.rng[L][a][s].lo;
+    }
+    const Rng seg = S.rng[L][a][s];
+    const uint32_t row = r + l;
+    const uint32_t *col = D.seg[s].cols[D.lvl_col[L]];
+    bool alive = row < seg.hi;
+    uint32_t v = 0;
+    if (alive) {
+        v = __ldg(col + row);
+        alive = row == seg.lo || __ldg(col + row - 1) != v;
+    }
+    if (alive && s == 1) {
+        Rng t = S.rng[L][a][0];
+        if (t.lo < t.hi) alive = narrow_first(D, 0, L, v, t) == 0;
+    }
+    const int leaf = (int)P.depth - 1;
+    const bool parents_level = L == leaf - 1;
+    for (uint32_t j = 0; j < P.nspec[L] && alive; ++j) {
+        const uint32_t b = P.spec[L][j];
+        const srdl_atom &A = P.atom[b];
+        const uint32_t slot = P.leaf_slot[b];
+        const bool keep = parents_level && slot != SRDL_NO_ATOM;
+        if (b == a && A.lvl_ncol[L] == 1 && !keep && A.nseg == 1) continue;
+        uint32_t tot = 0;
+        for (uint32_t q = 0; q < A.nseg; ++q) {
+            Rng t = S.rng[L][b][q];
+            if (t.lo < t.hi) tot += narrow(A, q, L, v, t);
+            else t.hi = t.lo;
+            if (keep) S.leaf[l][slot][q] = t;
+        }
+        if (A.negated ? (A.check_level == L && tot != 0) : tot == 0) alive = false;
+    }
+    if (parents_level && alive) {
+        // leaf sources not constrained at this level keep their ranges
+        for (uint32_t j = 0; j < P.nspec[leaf]; ++j) {
+            const uint32_t b = P.spec[leaf][j];
+            if (P.atom[b].lvl_ncol[L]) continue;
+            for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.leaf[l][j][q] = S.rng[L][b][q];
+        }
+    }
+    S.vals[L][l] = v;
+    const uint32_t m = __ballot_sync(kFull, alive);
+    if (l == 0) {
+        S.cur[L] = seg.hi - r > 32 ? r + 32 : seg.hi;
+        S.dseg[L] = (uint8_t)s;
+        S.mask[L] = parents_level ? 0u : m;
+    }
+    __syncwarp();
+    if (parents_level && m) leaf_batch<WRITE>(P, X, S, m, sink);
+    return true;
+}
+
+// Bind survivor `ln` of level L and derive the level L+1 ranges.
+__device__ __forceinline__ void descend(const srdl_plan &P, WarpState &S, int L, uint32_t ln) {
+    const uint32_t l = lane_id();
+    const uint32_t v = S.vals[L][ln];
+    if (l == 0) S.bind[L] = v;
+    for (uint32_t t = l; t < P.natoms * SRDL_MAX_SEGS; t += 32) {
+        const uint32_t a = t / SRDL_MAX_SEGS, s = t % SRDL_MAX_SEGS;
+        Rng r = S.rng[L][a][s];
+        const srdl_atom &A = P.atom[a];
+        if (A.lvl_ncol[L] && s < A.nseg && r.lo < r.hi) narrow(A, s, L, v, r);
+        S.rng[L + 1][a][s] = r;
+    }
+    __syncwarp();
+}
+
+// One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
+template <bool WRITE>
+__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t key,
+                         uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1, Sink<WRITE> &sink) {
+    const uint32_t l = lane_id();
+    const uint32_t a = l / SRDL_MAX_SEGS, s = l % SRDL_MAX_SEGS;
+    const bool mine = a < P.natoms;
+    uint32_t lo = 0, hi = 0;
+    bool has0 = false;
+    const srdl_atom &A = P.atom[mine ? a : 0];
+    if (mine && s < A.nseg) {
+        lo = A.seg[s].lo;
+        hi = A.seg[s].hi;
+    }
+    if (mine) has0 = A.lvl_ncol[0] != 0;
+    if (has0 && lo < hi) {
+        Rng t{lo, hi};
+        narrow_first(A, s, 0, key, t);
+        lo = t.lo;
+        hi = t.hi;
+    }
+    const uint32_t n_here = hi - lo;
+    const uint32_t n0 = __shfl_sync(kFull, n_here, l & ~1u);
+    if (mine && (a == P.outer || a == P.inner)) {
+        const uint64_t q0 = a == P.outer ? r0 : c0;
+        const uint64_t q1 = a == P.outer ? r1 : c1;
+        uint64_t f, e;
+        if (s == 0) {
+            f = q0 < n0 ? q0 : n0;
+            e = q1 < n0 ? q1 : n0;
+        } else {
+            f = q0 > n0 ? q0 - n0 : 0;
+            e = q1 > n0 ? q1 - n0 : 0;
+            if (f > n_here) f = n_here;
+            if (e > n_here) e = n_here;
+        }
+        hi = lo + (uint32_t)e;
+        lo = lo + (uint32_t)f;
+    }
+    if (has0 && A.lvl_ncol[0] > 1 && lo < hi) {
+        for (int c = A.lvl_col[0] + 1; c < A.lvl_col[0] + A.lvl_ncol[0] && lo < hi; ++c) {
+            const uint32_t *col = A.seg[s].cols[c];
+            uint32_t x = lbound(col, lo, hi, key);
+            hi = ubound(col, x, hi, key);
+            lo = x;
+        }
+        if (lo > hi) hi = lo;
+    }
+    const uint32_t len = hi - lo;
+    const uint32_t tot = len + __shfl_xor_sync(kFull, len, 1);
+    bool dead = false;
+    if (mine && s == 0 && has0) dead = A.negated ? (A.check_level == 0 && tot != 0) : tot == 0;
+    if (mine) S.rng[1][a][s] = Rng{lo, hi};
+    if (__any_sync(kFull, dead)) return;
+    __syncwarp();
+    if (P.depth == 1) {
+        sink.emit(P, X, S, l == 0, 0, key, 0);
+        return;
+    }
+    if (l == 0) {
+        S.bind[0] = key;
+        S.vals[0][0] = key;
+    }
+    if (P.depth == 2) {
+        for (uint32_t t = l; t < P.nspec[1] * SRDL_MAX_SEGS; t += 32) {
+            const uint32_t j = t / SRDL_MAX_SEGS, q = t % SRDL_MAX_SEGS;
+            S.leaf[0][j][q] = S.rng[1][P.spec[1][j]][q];
+        }
+        __syncwarp();
+        leaf_batch<WRITE>(P, X, S, 1u, sink);
+        return;
+    }
+    __syncwarp();
+    // DFS over levels 1..m-2; level m-2 hands its survivors to leaf_batch
+    int L = 1;
+    open_level(P, S, L);
+    while (true) {
+        const uint32_t m = S.mask[L];
+        if (m == 0) {
+            if (load_chunk<WRITE>(P, X, S, L, sink)) continue;
+            if (L == 1) break;
+            --L;
+            continue;
+        }
+        const uint32_t ln = __ffs(m) - 1;
+        __syncwarp();
+        if (l == 0) S.mask[L] = m & (m - 1);
+        descend(P, S, L, ln);
+        ++L;
+        open_level(P, S, L);
+    }
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kJoinWarps * 32)
+    wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X) {
+    __shared__ WarpState states[kJoinWarps];
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint32_t w = blockIdx.x * kJoinWarps + wib;
+    if (w >= X.nwarps) return;
+    WarpState &S = states[wib];
+    const uint64_t K = X.nkeys;
+    const uint64_t T = K ? X.prefix[K - 1] : 0;
+    const uint64_t step = (T + X.nwarps - 1) / X.nwarps;
+    uint64_t bs = (uint64_t)w * step, be = bs + step;
+    if (bs > T) bs = T;
+    if (be > T) be = T;
+    Sink<WRITE> sink{0, WRITE ? X.warp_offsets[w] : 0};
+    if (bs < be) {
+        // kappa: first key whose inclusive prefix exceeds bs
+        uint64_t lo = 0, hi = K;
+        while (lo < hi) {
+            uint64_t mid = (lo + hi) >> 1;
+            if (X.prefix[mid] <= bs)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        for (uint64_t k = lo; k < K; ++k) {
+            const uint64_t start = k ? X.prefix[k - 1] : 0;
+            if (start >= be) break;
+            const uint64_t end = X.prefix[k];
+            const uint64_t u0 = (bs > start ? bs : start) - start;
+            const uint64_t u1 = (be < end ? be : end) - start;
+            if (u0 >= u1) continue;
+            const uint64_t d2 = X.d2[k];
+            const uint32_t key = X.keys[k];
+            uint64_t ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
+            if (ra == rb) {
+                run_rect<WRITE>(P, X, S, key, ra, ra + 1, ca, cb, sink);
+                continue;
+            }
+            if (ca) {
+                run_rect<WRITE>(P, X, S, key, ra, ra + 1, ca, d2, sink);
+                ++ra;
+            }
+            if (ra < rb) run_rect<WRITE>(P, X, S, key, ra, rb, 0, d2, sink);
+            if (cb) run_rect<WRITE>(P, X, S, key, rb, rb + 1, 0, cb, sink);
+        }
+    }
+    if (lane_id() == 0) {
+        if (WRITE) {
+            if (sink.n != X.warp_counts[w]) atomicExch(X.error, 1u);
+        } else {
+            X.warp_counts[w] = sink.n;
+        }
+    }
+}
+
+static void check_plan(const srdl_plan *P, const srdl_exec *X) {
+    SRDL_REQUIRE(P->depth >= 1 && P->depth <= SRDL_MAX_LEVELS, "plan depth %u unsupported", P->depth);
+    SRDL_REQUIRE(P->natoms >= 1 && P->natoms <= SRDL_MAX_ATOMS, "plan has %u atoms", P->natoms);
+    SRDL_REQUIRE(P->head_arity <= SRDL_MAX_HEAD, "head arity %u", P->head_arity);
+    SRDL_REQUIRE(P->nspec[P->depth - 1] <= SRDL_MAX_LEAF_SPECS, "leaf level has %u sources (max %d)",
+                 P->nspec[P->depth - 1], SRDL_MAX_LEAF_SPECS);
+    SRDL_REQUIRE(X->nwarps >= 1, "nwarps must be >= 1");
+}
+
+}  // namespace srdl
+
+using namespace srdl;
+
+extern "C" {
+
+int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
+    return guarded([&] {
+        check_plan(plan, ex);
+        cudaStream_t s = (cudaStream_t)stream;
+        const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
+        wcoj_kernel<false><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u64(ex->warp_counts, ex->warp_offsets, ex->nwarps, ex->total, s);
+    });
+}
+
+int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
+    return guarded([&] {
+        check_plan(plan, ex);
+        cudaStream_t s = (cudaStream_t)stream;
+        const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
+        wcoj_kernel<true><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,380 @@
+"""ctypes binding to libsrdl.so (the C ABI in include/srdl.h) + buffer helpers.
+
+This is the only module that talks to the native library. Device buffers
+are torch tensors (PyTorch is used purely as the device allocator and stream
+provider); every call passes raw pointers, row counts and the current CUDA
+stream. There is no CPU fallback: if the library or a CUDA device is
+missing, `lib()` raises DeviceUnavailable.
+
+Layout conventions
+  * a row set is a 2-D uint32 tensor of shape (arity, n): row-major over
+    columns, so column c is the contiguous vector t[c] (SoA);
+  * 64-bit unsigned device arrays (prefix sums, counts) are int64 tensors.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .faults import DeviceUnavailable, InternalError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsrdl.so")
+
+MAX_ATOMS = 12
+MAX_LEVELS = 12
+MAX_COLS = 8
+MAX_HEAD = 12
+MAX_SEGS = 2
+MAX_LEAF_SPECS = 6
+NO_ATOM = 255
+NO_SYMBOL = 0xFFFFFFFF
+
+U32 = torch.uint32
+U64 = torch.int64  # bit pattern of uint64 device arrays
+
+
+class Segment(C.Structure):
+    _fields_ = [("cols", C.c_void_p * MAX_COLS), ("lo", C.c_uint32), ("hi", C.c_uint32)]
+
+
+class AtomDesc(C.Structure):
+    _fields_ = [
+        ("seg", Segment * MAX_SEGS),
+        ("nseg", C.c_uint32),
+        ("negated", C.c_uint32),
+        ("arity", C.c_uint32),
+        ("nconst", C.c_uint32),
+        ("check_level", C.c_int32),
+        ("lvl_col", C.c_uint8 * MAX_LEVELS),
+        ("lvl_ncol", C.c_uint8 * MAX_LEVELS),
+    ]
+
+
+class PlanDesc(C.Structure):
+    _fields_ = [
+        ("depth", C.c_uint32),
+        ("natoms", C.c_uint32),
+        ("outer", C.c_uint32),
+        ("inner", C.c_uint32),
+        ("head_arity", C.c_uint32),
+        ("head_level", C.c_int32 * MAX_HEAD),
+        ("head_const", C.c_uint32 * MAX_HEAD),
+        ("nspec", C.c_uint32 * MAX_LEVELS),
+        ("spec", (C.c_uint8 * MAX_ATOMS) * MAX_LEVELS),
+        ("leaf_slot", C.c_uint8 * MAX_ATOMS),
+        ("atom", AtomDesc * MAX_ATOMS),
+    ]
+
+
+class ExecDesc(C.Structure):
+    _fields_ = [
+        ("keys", C.c_void_p),
+        ("d2", C.c_void_p),
+        ("prefix", C.c_void_p),
+        ("nkeys", C.c_uint64),
+        ("nwarps", C.c_uint32),
+        ("warp_counts", C.c_void_p),
+        ("warp_offsets", C.c_void_p),
+        ("total", C.c_void_p),
+        ("out", C.c_void_p * MAX_HEAD),
+        ("error", C.c_void_p),
+        ("bitmap", C.c_void_p),
+    ]
+
+
+_LIB = None
+_SIGNATURES = {
+    "srdl_version": (C.c_int, []),
+    "srdl_last_error": (C.c_char_p, []),
+    "srdl_sm_count": (C.c_int, []),
+    "srdl_launch_count": (C.c_uint64, []),
+    "srdl_sort_dedup": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_compute_delta": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
+         C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_merge": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p],
+    ),
+    "srdl_is_sorted_strict": (
+        C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.POINTER(C.c_int), C.c_void_p]
+    ),
+    "srdl_gather": (
+        C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
+    ),
+    "srdl_histogram": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_histogram_merge": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+         C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_narrow_prefix": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint32, C.POINTER(C.c_uint64),
+         C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_root_work": (
+        C.c_int,
+        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,
+         C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "srdl_wcoj_count": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
+    "srdl_wcoj_materialize": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
+    "srdl_gen_rmat": (
+        C.c_int,
+        [C.c_uint32, C.c_uint64, C.c_float, C.c_float, C.c_float, C.c_uint64, C.c_void_p,
+         C.c_void_p, C.c_void_p],
+    ),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    """Open libsrdl.so and declare its C signatures (no CUDA needed)."""
+    if not os.path.exists(path):
+        raise DeviceUnavailable(
+            f"{path} is missing: build it with `python -m paper_2604_20073_b200.build` "
+            "(the engine has no CPU fallback)"
+        )
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib():
+    """The loaded library, after checking that a CUDA device is usable."""
+    global _LIB
+    if _LIB is None:
+        if not torch.cuda.is_available():
+            raise DeviceUnavailable("no CUDA device: the sm_100a engine has no CPU fallback")
+        _LIB = load_library()
+        if _LIB.srdl_version() != 1:
+            raise DeviceUnavailable("libsrdl.so version mismatch; rebuild it")
+    return _LIB
+
+
+def device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = _LIB.srdl_last_error().decode(errors="replace") if _LIB else "?"
+        raise InternalError(f"{what} failed ({rc}): {msg}")
+
+
+_SM = None
+
+
+def sm_count() -> int:
+    global _SM
+    if _SM is None:
+        n = lib().srdl_sm_count()
+        _SM = n if n > 0 else 148
+    return _SM
+
+
+# ---------------------------------------------------------------- buffers
+
+
+def empty_rows(arity: int, n: int = 0) -> torch.Tensor:
+    return torch.empty((arity, n), dtype=U32, device=device())
+
+
+def to_device_rows(cols) -> torch.Tensor:
+    """Host columns (sequence of 1-D arrays) -> (arity, n) uint32 device tensor."""
+    import numpy as np
+
+    arr = np.ascontiguousarray(np.stack([np.asarray(c, dtype=np.uint32) for c in cols]))
+    return torch.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def nrows(rows: torch.Tensor) -> int:
+    return rows.shape[1]
+
+
+def col_ptrs(rows: torch.Tensor, order=None):
+    """ctypes array of column pointers (optionally permuted to `order`)."""
+    arity = rows.shape[0]
+    order = range(arity) if order is None else order
+    base = rows.data_ptr()
+    stride = rows.stride(0) * 4
+    if rows.shape[1] and rows.stride(1) != 1:
+        raise InternalError("row set columns must be contiguous")
+    ptrs = (C.c_void_p * MAX_COLS)()
+    for k, c in enumerate(order):
+        ptrs[k] = base + c * stride
+    return ptrs
+
+
+def sym_bits(nsym: int) -> int:
+    return max(1, int(nsym - 1).bit_length()) if nsym > 1 else 1
+
+
+# ------------------------------------------------------------- operations
+
+
+def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None) -> torch.Tensor:
+    """Distinct rows sorted lexicographically (columns taken in `order`)."""
+    arity, n = rows.shape
+    order = list(range(arity)) if order is None else list(order)
+    out = empty_rows(len(order), n)
+    if n == 0:
+        return out
+    got = C.c_uint64(0)
+    check(
+        lib().srdl_sort_dedup(col_ptrs(rows, order), len(order), n, bits, col_ptrs(out),
+                              C.byref(got), stream_handle()),
+        "sort_dedup",
+    )
+    return _trim(out, got.value)
+
+
+def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
+    """sort_dedup(rows) minus the rows of the given sorted segments."""
+    arity, n = rows.shape
+    out = empty_rows(arity, n)
+    if n == 0:
+        return out
+    segs = [s for s in segments if nrows(s)]
+    seg_ptr_arrays = [col_ptrs(s) for s in segs]
+    seg_cols = (C.c_void_p * MAX_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
+    seg_rows = (C.c_uint64 * MAX_SEGS)(*[nrows(s) for s in segs])
+    got = C.c_uint64(0)
+    check(
+        lib().srdl_compute_delta(col_ptrs(rows), arity, n, bits, seg_cols, seg_rows, len(segs),
+                                 col_ptrs(out), C.byref(got), stream_handle()),
+        "compute_delta",
+    )
+    return _trim(out, got.value)
+
+
+def merge(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Sorted union of two sorted, disjoint row sets."""
+    arity = a.shape[0]
+    na, nb = nrows(a), nrows(b)
+    if nb == 0:
+        return a
+    if na == 0:
+        return b
+    out = empty_rows(arity, na + nb)
+    check(
+        lib().srdl_merge(col_ptrs(a), na, col_ptrs(b), nb, arity, col_ptrs(out), stream_handle()),
+        "merge",
+    )
+    return out
+
+
+def is_sorted_strict(rows: torch.Tensor) -> bool:
+    ok = C.c_int(1)
+    arity, n = rows.shape
+    if n <= 1:
+        return True
+    check(lib().srdl_is_sorted_strict(col_ptrs(rows), arity, n, C.byref(ok), stream_handle()),
+          "is_sorted_strict")
+    return bool(ok.value)
+
+
+def gather(rows: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    arity = rows.shape[0]
+    n = idx.numel()
+    out = empty_rows(arity, n)
+    if n:
+        check(lib().srdl_gather(col_ptrs(rows), arity, idx.data_ptr(), n, col_ptrs(out),
+                                stream_handle()), "gather")
+    return out
+
+
+def histogram(col: torch.Tensor):
+    """(keys u32, degrees u32, inclusive prefix i64) of a sorted column."""
+    n = col.numel()
+    keys = torch.empty(n, dtype=U32, device=device())
+    deg = torch.empty(n, dtype=U32, device=device())
+    prefix = torch.empty(n, dtype=U64, device=device())
+    if n == 0:
+        return keys, deg, prefix
+    k = C.c_uint64(0)
+    check(lib().srdl_histogram(col.data_ptr(), n, keys.data_ptr(), deg.data_ptr(), prefix.data_ptr(),
+                               C.byref(k), stream_handle()), "histogram")
+    K = k.value
+    return keys[:K], deg[:K], prefix[:K]
+
+
+def histogram_merge(ka, da, kb, db):
+    na, nb = ka.numel(), kb.numel()
+    n = na + nb
+    keys = torch.empty(n, dtype=U32, device=device())
+    deg = torch.empty(n, dtype=U32, device=device())
+    prefix = torch.empty(n, dtype=U64, device=device())
+    k = C.c_uint64(0)
+    check(lib().srdl_histogram_merge(ka.data_ptr(), da.data_ptr(), na, kb.data_ptr(), db.data_ptr(),
+                                     nb, keys.data_ptr(), deg.data_ptr(), prefix.data_ptr(),
+                                     C.byref(k), stream_handle()), "histogram_merge")
+    K = k.value
+    return keys[:K], deg[:K], prefix[:K]
+
+
+def narrow_prefix(rows: torch.Tensor, lo: int, hi: int, values) -> tuple:
+    """Rows within [lo, hi) whose leading columns equal `values`."""
+    if lo >= hi or not values:
+        return lo, hi
+    vals = (C.c_uint32 * MAX_COLS)(*values)
+    a, b = C.c_uint64(0), C.c_uint64(0)
+    sub = rows[:, lo:hi]
+    ptrs = (C.c_void_p * MAX_COLS)()
+    for c in range(len(values)):
+        ptrs[c] = sub[c].data_ptr()
+    check(lib().srdl_narrow_prefix(ptrs, hi - lo, vals, len(values), C.byref(a), C.byref(b),
+                                   stream_handle()), "narrow_prefix")
+    return lo + a.value, lo + b.value
+
+
+def root_work(okeys, odeg, ikeys=None, ideg=None):
+    """(d2 u32, inclusive work prefix i64) for an outer/inner histogram pair."""
+    nk = okeys.numel()
+    d2 = torch.empty(nk, dtype=U32, device=device())
+    prefix = torch.empty(nk, dtype=U64, device=device())
+    if nk == 0:
+        return d2, prefix
+    has_inner = ikeys is not None
+    check(lib().srdl_root_work(okeys.data_ptr(), odeg.data_ptr(), nk,
+                               ikeys.data_ptr() if has_inner and ikeys.numel() else None,
+                               ideg.data_ptr() if has_inner and ideg.numel() else None,
+                               ikeys.numel() if has_inner else 0, int(has_inner), d2.data_ptr(),
+                               prefix.data_ptr(), stream_handle()), "root_work")
+    return d2, prefix
+
+
+def gen_rmat(scale: int, nedges: int, a=0.57, b=0.19, c=0.19, seed=1) -> torch.Tensor:
+    out = empty_rows(2, nedges)
+    check(lib().srdl_gen_rmat(scale, nedges, a, b, c, seed, out[0].data_ptr(), out[1].data_ptr(),
+                              stream_handle()), "gen_rmat")
+    return out
+
+
+def _trim(rows: torch.Tensor, n: int) -> torch.Tensor:
+    """Exact-size result: a view when little is wasted, else a compact copy."""
+    cap = rows.shape[1]
+    if n == cap:
+        return rows
+    if n >= cap // 2:
+        return rows[:, :n]
+    return rows[:, :n].clone()

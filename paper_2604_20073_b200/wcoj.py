@@ -1,0 +1,368 @@
+"""Plan execution on the device: histogram -> count -> allocate -> materialize.
+
+Mirrors the reference executor API (reference: pkg/src/flatlog/executor.py:
+45-549: WorkPartition, decode_workunit, build_partition, count_pass,
+materialize_pass, PlanExecution, execute_plan) with every data-touching
+step running in libsrdl:
+
+* prepare    resolve each plan atom to an index version (full / delta, per
+             column order) and narrow it on its constant columns;
+* histogram  root work space: outer histogram (maintained incrementally by
+             the storage layer, or rebuilt over a constant-narrowed range),
+             inner degrees d2 and the inclusive prefix of outer * d2;
+* count      csrc/wcoj.cu count kernel over p warp slices + exclusive scan;
+* allocate   one exactly-sized output buffer (the only host sync);
+* materialize the same walk writing at the per-warp offsets.
+
+`p` is the reference's worker count. On the device the slices are warps:
+the kernel uses max(p, DEVICE_WARPS) slices; results do not depend on it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import audit
+from . import device as dev
+from .compiler import DELTA, FULL, JoinPlan
+from .faults import InternalError
+from .partition import WorkPartition, decode_workunit, encode_workunit, rectangles  # noqa: F401
+from .syntax import VAR
+
+WARPS_PER_SM = 28  # 7 resident CTAs x 4 warps (30 KB shared memory each)
+
+
+def device_warps(p: int = 1) -> int:
+    return max(int(p), dev.sm_count() * WARPS_PER_SM)
+
+
+def _resolve(store, pa):
+    state = store[pa.relation]
+    return state.full(pa.column_order) if pa.version == FULL else state.delta(pa.column_order)
+
+
+class Prepared:
+    """Read-only device view of one plan execution's sources."""
+
+    __slots__ = ("plan", "rels", "segs", "ok", "head_resolved", "_desc")
+
+    def __init__(self, plan, rels, segs, ok, head_resolved):
+        self.plan = plan
+        self.rels = rels
+        self.segs = segs  # per atom: [(rows tensor, lo, hi), ...] body first
+        self.ok = ok
+        self.head_resolved = head_resolved
+        self._desc = None
+
+    def descriptor(self) -> dev.PlanDesc:
+        if self._desc is None:
+            self._desc = encode_plan(self)
+        return self._desc
+
+
+def prepare(plan: JoinPlan, store, interner) -> Prepared:
+    ok = True
+    rels, segs = [], []
+    for pa in plan.atoms:
+        rel = _resolve(store, pa)
+        src = [(t, 0, t.shape[1]) for t in rel.segments()]
+        if pa.n_const:
+            ids = [interner.lookup(c) for c in pa.const_values]
+            if any(i is None for i in ids):
+                src = []
+            else:
+                narrowed = []
+                for t, lo, hi in src:
+                    a, b = dev.narrow_prefix(t, lo, hi, ids)
+                    if a < b:
+                        narrowed.append((t, a, b))
+                src = narrowed
+        rels.append(rel)
+        segs.append(src)
+        if not pa.negated and not src:
+            ok = False
+        if pa.negated and pa.check_level == -1 and src:
+            ok = False
+    head = tuple((True, x) if kind == VAR else (False, interner.intern(x)) for kind, x in plan.head_cols)
+    return Prepared(plan, rels, segs, ok, head)
+
+
+def encode_plan(prep: Prepared) -> dev.PlanDesc:
+    """JoinPlan + resolved segments -> the fixed-size srdl_plan descriptor."""
+    plan = prep.plan
+    if plan.depth > dev.MAX_LEVELS or len(plan.atoms) > dev.MAX_ATOMS:
+        raise InternalError(f"plan {plan.plan_id}: {plan.depth} variables / {len(plan.atoms)} atoms "
+                            f"exceed the device limits ({dev.MAX_LEVELS}/{dev.MAX_ATOMS})")
+    if plan.head_arity > dev.MAX_HEAD:
+        raise InternalError(f"plan {plan.plan_id}: head arity {plan.head_arity} > {dev.MAX_HEAD}")
+    d = dev.PlanDesc()
+    d.depth = plan.depth
+    d.natoms = len(plan.atoms)
+    d.outer = plan.outer_atom if plan.outer_atom is not None else dev.NO_ATOM
+    d.inner = plan.inner_atom if plan.inner_atom is not None else dev.NO_ATOM
+    d.head_arity = plan.head_arity
+    for h, (is_var, x) in enumerate(prep.head_resolved):
+        d.head_level[h] = x if is_var else -1
+        d.head_const[h] = 0 if is_var else x
+    for lvl, specs in enumerate(plan.narrow_specs):
+        d.nspec[lvl] = len(specs)
+        for j, (a, _cols) in enumerate(specs):
+            d.spec[lvl][j] = a
+    for a in range(dev.MAX_ATOMS):
+        d.leaf_slot[a] = dev.NO_ATOM
+    if plan.depth:
+        leaf_specs = plan.narrow_specs[plan.depth - 1]
+        if len(leaf_specs) > dev.MAX_LEAF_SPECS:
+            raise InternalError(f"plan {plan.plan_id}: {len(leaf_specs)} sources on the last variable "
+                                f"(device limit {dev.MAX_LEAF_SPECS})")
+        for j, (a, _cols) in enumerate(leaf_specs):
+            d.leaf_slot[a] = j
+    for a, pa in enumerate(plan.atoms):
+        if pa.arity > dev.MAX_COLS:
+            raise InternalError(f"relation {pa.relation}: arity {pa.arity} > {dev.MAX_COLS}")
+        ad = d.atom[a]
+        src = prep.segs[a]
+        ad.nseg = len(src)
+        for s, (rows, lo, hi) in enumerate(src):
+            ptrs = dev.col_ptrs(rows)
+            for c in range(pa.arity):
+                ad.seg[s].cols[c] = ptrs[c]
+            ad.seg[s].lo = lo
+            ad.seg[s].hi = hi
+        ad.negated = int(pa.negated)
+        ad.arity = pa.arity
+        ad.nconst = pa.n_const
+        ad.check_level = pa.check_level
+        for lvl, cols in pa.levels_with_columns().items():
+            ad.lvl_col[lvl] = cols[0]
+            ad.lvl_ncol[lvl] = len(cols)
+    return d
+
+
+class DevicePartition:
+    """Root work space on the device (keys, outer degrees, d2, prefix)."""
+
+    __slots__ = ("keys", "outer_degrees", "d2", "prefix", "p", "nwarps", "_total")
+
+    def __init__(self, keys, outer_degrees, d2, prefix, p):
+        self.keys = keys
+        self.outer_degrees = outer_degrees
+        self.d2 = d2
+        self.prefix = prefix
+        self.p = p
+        self.nwarps = device_warps(p)
+        self._total = None
+
+    @classmethod
+    def empty(cls, p: int) -> "DevicePartition":
+        z32 = torch.empty(0, dtype=dev.U32, device=dev.device())
+        return cls(z32, z32, z32, torch.empty(0, dtype=dev.U64, device=dev.device()), p)
+
+    @property
+    def nkeys(self) -> int:
+        return self.keys.numel()
+
+    @property
+    def total(self) -> int:
+        if self._total is None:
+            self._total = int(self.prefix[-1].item()) if self.nkeys else 0
+        return self._total
+
+    def to_host(self, p: int | None = None) -> WorkPartition:
+        """The same partition in the reference's numpy form."""
+        return WorkPartition(
+            self.keys.cpu().numpy(),
+            self.outer_degrees.cpu().numpy().astype(np.int64),
+            self.d2.cpu().numpy().astype(np.int64),
+            p or self.p,
+        )
+
+    def slice_sizes(self) -> list:
+        t, n = self.total, self.nwarps
+        step = -(-t // n) if t else 0
+        return [max(0, min((w + 1) * step, t) - min(w * step, t)) for w in range(n)]
+
+
+def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None, interner=None):
+    if p < 1:
+        raise InternalError("worker count must be >= 1")
+    if prep is None:
+        prep = prepare(plan, store, interner)
+    if plan.depth == 0 or not prep.ok:
+        return DevicePartition.empty(p)
+    outer = plan.atoms[plan.outer_atom]
+    if outer.n_const == 0:
+        hist = prep.rels[plan.outer_atom].hist
+        okeys, odeg = hist.keys, hist.degrees
+    else:
+        from .columns import Histogram
+
+        h = Histogram.empty()
+        for rows, lo, hi in prep.segs[plan.outer_atom]:
+            h = h.updated(rows[outer.n_const, lo:hi].contiguous())
+        okeys, odeg = h.keys, h.degrees
+    if okeys.numel() == 0:
+        return DevicePartition.empty(p)
+    if plan.inner_atom is not None:
+        ih = prep.rels[plan.inner_atom].hist
+        d2, prefix = dev.root_work(okeys, odeg, ih.keys, ih.degrees)
+    else:
+        d2, prefix = dev.root_work(okeys, odeg)
+    return DevicePartition(okeys, odeg, d2, prefix, p)
+
+
+@dataclass
+class CountResult:
+    """Per-slice counts (device), their exclusive prefix and the total."""
+
+    warp_counts: torch.Tensor
+    warp_offsets: torch.Tensor
+    total_dev: torch.Tensor
+    _total: int | None = None
+
+    @classmethod
+    def constant(cls, n_slices: int, first: int) -> "CountResult":
+        d = dev.device()
+        counts = torch.zeros(n_slices, dtype=dev.U64, device=d)
+        counts[0] = first
+        offs = torch.zeros(n_slices, dtype=dev.U64, device=d)
+        offs[1:] = first
+        return cls(counts, offs, torch.full((1,), first, dtype=dev.U64, device=d), first)
+
+    @property
+    def total(self) -> int:
+        if self._total is None:
+            self._total = int(self.total_dev.item())
+        return self._total
+
+    @property
+    def tc(self) -> np.ndarray:
+        return self.warp_counts.cpu().numpy()
+
+    @property
+    def offsets(self) -> np.ndarray:
+        return self.warp_offsets.cpu().numpy()
+
+
+def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=None,
+               bitmap=None) -> dev.ExecDesc:
+    x = dev.ExecDesc()
+    x.keys = partition.keys.data_ptr()
+    x.d2 = partition.d2.data_ptr()
+    x.prefix = partition.prefix.data_ptr()
+    x.nkeys = partition.nkeys
+    x.nwarps = partition.nwarps
+    x.warp_counts = counts.warp_counts.data_ptr()
+    x.warp_offsets = counts.warp_offsets.data_ptr()
+    x.total = counts.total_dev.data_ptr()
+    if out is not None:
+        for h in range(out.shape[0]):
+            x.out[h] = out[h].data_ptr()
+    if error is not None:
+        x.error = error.data_ptr()
+    if bitmap is not None:
+        x.bitmap = bitmap.data_ptr()
+    return x
+
+
+def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> CountResult:
+    """Read-only pass: exact per-slice output counts, nothing written."""
+    if prep is None:
+        prep = prepare(plan, store, interner)
+    n = partition.nwarps
+    if plan.depth == 0:
+        return CountResult.constant(n, 1 if prep.ok else 0)
+    if not prep.ok or partition.nkeys == 0:
+        return CountResult.constant(n, 0)
+    d = dev.device()
+    counts = CountResult(
+        torch.empty(n, dtype=dev.U64, device=d),
+        torch.empty(n, dtype=dev.U64, device=d),
+        torch.empty(1, dtype=dev.U64, device=d),
+    )
+    desc = prep.descriptor()
+    x = _exec_desc(partition, counts)
+    dev.check(dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x), dev.stream_handle()), "wcoj_count")
+    return counts
+
+
+def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep=None, interner=None,
+                     pool=None, error=None, bitmap=None):
+    """Second pass: the same walk, writing every slice's tuples at its offset."""
+    if prep is None:
+        prep = prepare(plan, store, interner)
+    total = counts.total
+    if total == 0:
+        return out_cols
+    if plan.depth == 0:
+        vals = [x for _, x in prep.head_resolved]
+        out_cols[:, 0] = torch.tensor(vals, dtype=torch.int64).to(torch.uint32).to(out_cols.device)
+        if bitmap is not None:
+            bitmap += 1
+        return out_cols
+    own_flag = error is None
+    if own_flag:
+        error = torch.zeros(1, dtype=torch.int32, device=dev.device())
+    desc = prep.descriptor()
+    x = _exec_desc(partition, counts, out_cols, error, bitmap)
+    dev.check(dev.lib().srdl_wcoj_materialize(C.byref(desc), C.byref(x), dev.stream_handle()),
+              "wcoj_materialize")
+    if own_flag and int(error.item()):
+        raise InternalError(f"plan {plan.plan_id}: materialized tuple count diverged from the count pass")
+    return out_cols
+
+
+class PlanExecution:
+    """One plan's pipeline split into phases so schedulers can interleave
+    the same phase of independent plans (reference executor.PlanExecution)."""
+
+    def __init__(self, plan, store, p, interner, pool=None):
+        self.plan = plan
+        self.store = store
+        self.p = p
+        self.interner = interner
+        self.prep = None
+        self.partition = None
+        self.counts = None
+        self.out = None
+        self.error = None
+        self.bitmap = None
+        self.aux_peak = 0
+
+    def histogram(self):
+        self.prep = prepare(self.plan, self.store, self.interner)
+        self.partition = build_partition(self.plan, self.store, self.p, self.prep)
+        return self.partition
+
+    def count(self) -> CountResult:
+        self.counts = count_pass(self.plan, self.store, self.partition, self.prep)
+        return self.counts
+
+    def allocate(self, out=None):
+        total = self.counts.total
+        self.out = out if out is not None else dev.empty_rows(self.plan.head_arity, total)
+        self.aux_peak = max(self.aux_peak, total)
+        if audit.enabled:
+            self.bitmap = torch.zeros(total, dtype=torch.int32, device=dev.device())
+        return self.out
+
+    def materialize(self, error=None):
+        materialize_pass(self.plan, self.store, self.partition, self.counts, self.out, self.prep,
+                         error=error, bitmap=self.bitmap)
+        if audit.enabled:
+            audit.record_execution(self)
+        return self.out
+
+
+def execute_plan(plan, store, p, interner, pool=None) -> torch.Tensor:
+    """Histogram, count, allocate once, materialize; returns the staged head
+    tuples as a (head_arity, total) device tensor (attribute order)."""
+    run = PlanExecution(plan, store, p, interner, pool)
+    run.histogram()
+    run.count()
+    run.allocate()
+    return run.materialize()

@@ -1,0 +1,124 @@
+"""Device storage kernels (csrc/sort.cu, csrc/setops.cu) against the
+reference's golden storage fixtures and the numpy oracle at scale."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import storage as ost  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2604_20073_b200 import device
+
+    device.lib()
+    return device
+
+
+def to_dev(rows, arity):
+    from paper_2604_20073_b200 import device
+
+    arr = np.asarray(rows, dtype=np.uint32).reshape(-1, arity).T.copy()
+    return torch.from_numpy(arr).to(device.device())
+
+
+def host(t):
+    return t.cpu().numpy().astype(np.int64).T
+
+
+def test_sort_dedup_golden(dev, golden):
+    for case in golden("storage.json")["sort_dedup"]:
+        rows = to_dev(case["rows"], case["arity"])
+        for bits in (5, 32):
+            got = dev.sort_dedup(rows, bits, order=case["order"])
+            assert host(got).tolist() == case["out"]
+
+
+def test_compute_delta_golden(dev, golden):
+    for case in golden("storage.json")["compute_delta"]:
+        a = case["arity"]
+        segs = [to_dev(case["body"], a), to_dev(case["head"], a)]
+        got = dev.compute_delta(to_dev(case["new"], a), segs, 5)
+        assert host(got).tolist() == case["out"]
+
+
+def test_merge_sequences_golden(dev, golden):
+    from paper_2604_20073_b200.columns import ColumnarRelation, as_tuples
+
+    for case in golden("storage.json")["merge"]:
+        a = case["arity"]
+        rel = ColumnarRelation.empty(a, case["order"])
+        for step in case["steps"]:
+            rel = rel.merge_delta(to_dev(step["delta"], a), flush_limit=case["flush"])
+            assert [list(r) for r in as_tuples(rel.head)] == step["head"]
+            assert [list(r) for r in as_tuples(rel.body)] == step["body"]
+            assert rel.hist.keys.cpu().tolist() == step["hist_keys"]
+            assert rel.hist.degrees.cpu().tolist() == step["hist_degrees"]
+            assert rel.hist.prefix.cpu().tolist() == step["hist_prefix"]
+            rel.check_invariants()
+
+
+def test_histogram_updates_golden(dev, golden):
+    from paper_2604_20073_b200.columns import Histogram
+
+    for seq in golden("storage.json")["histogram"]:
+        h = Histogram.empty()
+        for step in seq:
+            col = torch.tensor(step["delta"], dtype=torch.int64).to(torch.uint32).to(dev.device())
+            h = h.updated(col)
+            assert h.keys.cpu().tolist() == step["keys"]
+            assert h.degrees.cpu().tolist() == step["degrees"]
+            assert h.prefix.cpu().tolist() == step["prefix"]
+
+
+@pytest.mark.parametrize("arity,bits,n,domain", [
+    (1, 20, 1_000_003, 1 << 20),
+    (2, 24, 3_000_000, 1 << 12),
+    (3, 21, 2_000_000, 1 << 7),
+    (4, 32, 500_000, 1 << 32),       # 128-bit keys: chunked LSD with a row permutation
+    (5, 13, 700_000, 7),             # heavy duplication, 65 bits
+    (8, 32, 100_000, 3),
+])
+def test_sort_dedup_at_scale(dev, arity, bits, n, domain):
+    rng = np.random.default_rng(arity * 1000 + bits)
+    rows = rng.integers(0, domain, size=(n, arity), dtype=np.uint64).astype(np.int64)
+    got = dev.sort_dedup(to_dev(rows, arity), bits)
+    assert np.array_equal(host(got), ost.sort_dedup(rows))
+    assert dev.is_sorted_strict(got)
+
+
+def test_compute_delta_and_merge_at_scale(dev):
+    rng = np.random.default_rng(5)
+    full = ost.sort_dedup(rng.integers(0, 3000, size=(2_000_000, 2)))
+    head = ost.difference(ost.sort_dedup(rng.integers(3000, 3100, size=(20_000, 2))), full)
+    new = rng.integers(0, 3200, size=(1_500_000, 2))
+    want = ost.compute_delta(new, head, full)
+    got = dev.compute_delta(to_dev(new, 2), [to_dev(full, 2), to_dev(head, 2)], 12)
+    assert np.array_equal(host(got), want)
+    merged = dev.merge(to_dev(full, 2), got)
+    assert np.array_equal(host(merged), ost.merge_sorted(full, want))
+
+
+def test_histogram_at_scale(dev):
+    rng = np.random.default_rng(11)
+    col = np.sort(rng.zipf(1.3, size=3_000_000) % 100_000).astype(np.uint32)
+    keys, deg, prefix = dev.histogram(torch.from_numpy(col).to(dev.device()))
+    uk, cnt = np.unique(col, return_counts=True)
+    assert np.array_equal(keys.cpu().numpy(), uk)
+    assert np.array_equal(deg.cpu().numpy(), cnt)
+    assert np.array_equal(prefix.cpu().numpy(), np.cumsum(cnt))
+
+
+def test_empty_and_single_rows(dev):
+    e = to_dev([], 3)
+    assert dev.sort_dedup(e, 8).shape == (3, 0)
+    assert dev.compute_delta(e, [to_dev([(1, 2, 3)], 3)], 8).shape == (3, 0)
+    one = to_dev([(4, 5, 6)], 3)
+    assert host(dev.sort_dedup(one, 8)).tolist() == [[4, 5, 6]]
+    assert dev.compute_delta(one, [one], 8).shape[1] == 0
+    assert dev.is_sorted_strict(one)
+    top = to_dev([(0xFFFFFFFE, 0), (0, 0xFFFFFFFE), (0xFFFFFFFE, 0)], 2)
+    assert host(dev.sort_dedup(top, 32)).tolist() == [[0, 0xFFFFFFFE], [0xFFFFFFFE, 0]]

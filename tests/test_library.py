@@ -1,0 +1,72 @@
+"""The C-ABI library builds, loads without a GPU, and exports exactly what
+include/srdl.h declares; the ctypes descriptors match the C layout."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2604_20073_b200 import build as builder
+from paper_2604_20073_b200 import device as dev
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "srdl.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    builder.build()
+    return dev.load_library()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|uint64_t|const char \*)\s*(srdl_\w+)\(", text, re.M)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(dev._SIGNATURES), "ctypes signatures out of sync with srdl.h"
+
+
+def test_version_without_gpu(lib):
+    assert lib.srdl_version() == 1
+
+
+def test_descriptor_layout_matches_c(tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "srdl.h"\n'
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(srdl_segment),"
+        " sizeof(srdl_atom), sizeof(srdl_plan), sizeof(srdl_exec), offsetof(srdl_plan, atom),"
+        " offsetof(srdl_exec, bitmap)); return 0;}\n"
+    )
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.dirname(HEADER), str(src), "-o", str(exe)], check=True)
+    got = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
+    want = [
+        ctypes.sizeof(dev.Segment),
+        ctypes.sizeof(dev.AtomDesc),
+        ctypes.sizeof(dev.PlanDesc),
+        ctypes.sizeof(dev.ExecDesc),
+        dev.PlanDesc.atom.offset,
+        dev.ExecDesc.bitmap.offset,
+    ]
+    assert got == want
+    assert ctypes.sizeof(dev.PlanDesc) + ctypes.sizeof(dev.ExecDesc) < 4096  # kernel parameter space
+
+
+def test_engine_fails_loudly_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    from paper_2604_20073_b200 import DeviceUnavailable, Engine, parse
+
+    with pytest.raises(DeviceUnavailable):
+        Engine(parse(".decl R(a:symbol)\n"))
