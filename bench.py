@@ -1,0 +1,539 @@
+#!/usr/bin/env python
+"""Fixpoint benchmark on B200 (BASELINE.json: "fixpoint wall-time (s) and
+derived tuples/sec at 1/2/4/8 B200 vs CPU ref").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+                    [--impl ours|reference]
+
+A step is one complete evaluation through the public API: build an Engine
+for the workload's program, load its EDB columns, solve to fixpoint. The
+metric is derived tuples per second = |output IDB relation| / step time,
+aggregated over all ranks. Default workload = BASELINE configs[1]:
+triangle listing on a synthetic R-MAT graph, 2^20 nodes / 16M edges.
+
+value    inputs already resident in HBM when the timed region starts.
+e2e      same step through the public API with pinned HOST inputs: the H2D
+         copy of the EDB columns and the D2H read of the output relation are
+         inside the timed region.
+roofline the dominant kernel (WCOJ count/materialize), CUDA events on its
+         stream over the timed steps, algorithmic bytes / duration vs the
+         measured HBM copy bandwidth (MEASURED_PEAKS.json).
+cpu_baseline / --impl reference
+         the numpy oracle restatement of the reference algorithm on a bounded
+         sample of the same workload (a subset of root keys), 1 host core.
+
+Multi-GPU (torchrun): root keys are hash-partitioned across ranks (x mod N),
+each rank evaluates its partition with no data-path collective; the timing is
+the max over ranks (NCCL all-reduce on the timings only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+TRIANGLE = """
+.decl R(a:symbol, b:symbol)
+.decl S(a:symbol, b:symbol)
+.decl T(a:symbol, b:symbol)
+.decl Triangle(a:symbol, b:symbol, c:symbol)
+.input R
+.input S
+.input T
+.output Triangle
+Triangle(x, y, z) :- R(x, y), S(y, z), T(z, x).
+"""
+
+TC = """
+.decl Edge(a:symbol, b:symbol)
+.decl TC(a:symbol, b:symbol)
+.input Edge
+.output TC
+TC(x, y) :- Edge(x, y).
+TC(x, z) :- TC(x, y), Edge(y, z).
+"""
+
+
+# --------------------------------------------------------------------------
+# workloads
+
+
+class Workload:
+    name = ""
+    program = ""
+    output = ""
+    config: dict = {}
+
+    def generate(self):
+        """-> {relation: (2, n) uint32 device tensor} (this rank's share)."""
+        raise NotImplementedError
+
+    def algorithmic_bytes(self, inputs: dict, n_out: int) -> int:
+        raise NotImplementedError
+
+
+class TriangleRMAT(Workload):
+    name = "triangle-rmat"
+    program = TRIANGLE
+    output = "Triangle"
+
+    def __init__(self, scale=20, edges=16_000_000, seed=1, rank=0, world=1):
+        self.scale, self.nedges, self.seed, self.rank, self.world = scale, edges, seed, rank, world
+        self.config = {
+            "workload": f"triangle listing (cyclic 3-way WCOJ) on R-MAT scale {scale}",
+            "nodes": 1 << scale,
+            "rmat_edges_generated": edges,
+            "rmat_abc": [0.57, 0.19, 0.19],
+            "program": "Triangle(x,y,z) :- R(x,y), S(y,z), T(z,x) with R=S=T=E",
+        }
+
+    def edges(self):
+        import torch
+
+        from paper_2604_20073_b200 import device as dev
+
+        raw = dev.gen_rmat(self.scale, self.nedges, seed=self.seed)
+        keep = raw[0].view(torch.int32) != raw[1].view(torch.int32)
+        raw = raw[:, keep].contiguous()
+        return dev.sort_dedup(raw, self.scale)
+
+    def generate(self):
+        import torch
+
+        e = self.edges()
+        self.config["edges"] = int(e.shape[1])
+        if self.world == 1:
+            return {"R": e, "S": e, "T": e}
+        # hash partition on the root variable x: R(x, y) by column 0, T(z, x) by column 1
+        w = self.world
+        mine_r = (e[0].view(torch.int32) % w) == self.rank
+        mine_t = (e[1].view(torch.int32) % w) == self.rank
+        return {"R": e[:, mine_r].contiguous(), "S": e, "T": e[:, mine_t].contiguous()}
+
+    def algorithmic_bytes(self, inputs, n_out):
+        # each WCOJ launch must read the three sorted edge indexes once
+        # (2 x u32 per edge) and the root work arrays; materialize also
+        # writes 3 x u32 per derived tuple
+        edge_bytes = sum(8 * int(t.shape[1]) for t in inputs.values())
+        return edge_bytes, 12 * n_out
+
+
+class TCRandom(Workload):
+    name = "tc-random"
+    program = TC
+    output = "TC"
+
+    def __init__(self, nodes=10_000, edges=50_000, seed=1, rank=0, world=1):
+        self.nodes, self.nedges, self.seed, self.rank, self.world = nodes, edges, seed, rank, world
+        self.config = {"workload": f"transitive closure on a random digraph {nodes} nodes / {edges} edges"}
+
+    def generate(self):
+        import torch
+
+        from paper_2604_20073_b200 import device as dev
+
+        rng = np.random.default_rng(self.seed)
+        seen = set()
+        src, dst = [], []
+        while len(src) < self.nedges:
+            a, b = rng.integers(0, self.nodes, 2)
+            if a != b and (a, b) not in seen:
+                seen.add((a, b))
+                src.append(a)
+                dst.append(b)
+        e = torch.from_numpy(np.array([src, dst], dtype=np.uint32)).to(dev.device())
+        e = dev.sort_dedup(e, 32)
+        self.config["edges"] = int(e.shape[1])
+        if self.world > 1:
+            mine = (e[0].view(torch.int32) % self.world) == self.rank
+            return {"Edge": e, "_shard": e[:, mine]}
+        return {"Edge": e}
+
+    def algorithmic_bytes(self, inputs, n_out):
+        return 8 * sum(int(t.shape[1]) for t in inputs.values()), 8 * n_out
+
+
+WORKLOADS = {"triangle": TriangleRMAT, "tc": TCRandom}
+
+
+# --------------------------------------------------------------------------
+# measurement helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": mx,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def flush_l2(torch, buf):
+    buf.add_(1)  # 512 MiB write > 126 MB L2
+
+
+def load_profile_traffic(workload_name):
+    """dram bytes per launch of the dominant kernel from a committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "wcoj_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        d = json.load(fh)
+    return d.get(workload_name)
+
+
+# --------------------------------------------------------------------------
+# our arm
+
+
+def run_step(torch, Engine, parse, wl, inputs, host=False, out_pinned=None):
+    engine = Engine(parse(wl.program), schedule="stream")
+    for rel, t in inputs.items():
+        if rel.startswith("_"):
+            continue
+        engine.load_columns(rel, t)
+    summary = engine.solve()
+    n_out = summary.relations[wl.output]
+    if host:
+        rows = engine.relation_columns(wl.output)
+        dst = out_pinned[:, : rows.shape[1]] if out_pinned is not None else None
+        if dst is not None and dst.shape == rows.shape:
+            dst.copy_(rows, non_blocking=True)
+        else:
+            rows.cpu()
+        torch.cuda.current_stream().synchronize()
+    del engine
+    return n_out
+
+
+def bench_ours(args, rank, world, dist):
+    import torch
+
+    from paper_2604_20073_b200 import Engine, parse
+    from paper_2604_20073_b200 import device as dev
+    from paper_2604_20073_b200 import wcoj
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dev.lib()
+    wl = make_workload(args, rank, world)
+    inputs = wl.generate()
+    torch.cuda.synchronize()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev.device())
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also sizes the pinned output buffer)
+    n_out = 0
+    for _ in range(args.warmup):
+        n_out = run_step(torch, Engine, parse, wl, inputs)
+    # timed region: device events on the main stream, kernel events per launch
+    events = []
+    wcoj.KERNEL_EVENTS = events
+    launches0 = dev.lib().srdl_launch_count()
+    times = []
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
+        for _ in range(args.steps):
+            flush_l2(torch, flush)
+            barrier()
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            start.record()
+            n_out = run_step(torch, Engine, parse, wl, inputs)
+            end.record()
+            end.synchronize()
+            times.append(start.elapsed_time(end) / 1e3)
+    launches = dev.lib().srdl_launch_count() - launches0
+    wcoj.KERNEL_EVENTS = None
+    step_s = sum(times) / len(times)
+
+    # end-to-end through the public API with host inputs and output readback
+    pinned = {k: v.cpu().pin_memory() for k, v in inputs.items() if not k.startswith("_")}
+    out_pinned = torch.empty((3 if wl.output == "Triangle" else 2, n_out), dtype=torch.uint32,
+                             pin_memory=True)
+    h2d = sum(t.numel() * 4 for t in pinned.values())
+    e2e_times = []
+    for i in range(max(1, min(args.steps, 3))):
+        flush_l2(torch, flush)
+        barrier()
+        t0 = time.perf_counter()
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record()
+        run_step(torch, Engine, parse, wl, pinned, host=True, out_pinned=out_pinned)
+        end.record()
+        end.synchronize()
+        e2e_times.append(max(start.elapsed_time(end) / 1e3, time.perf_counter() - t0))
+    e2e_s = sum(e2e_times) / len(e2e_times)
+
+    # max over ranks
+    tot_out = n_out
+    if dist:
+        t = torch.tensor([step_s, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s, e2e_s = t.tolist()
+        c = torch.tensor([n_out], dtype=torch.int64, device="cuda")
+        dist.all_reduce(c)
+        tot_out = int(c.item())
+
+    # dominant kernel roofline
+    kern = {}
+    for name, a, b in events:
+        kern.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
+    roofline = None
+    if kern:
+        name = max(kern, key=lambda k: sum(kern[k]))
+        per_launch = sum(kern[name]) / len(kern[name])
+        in_bytes, out_bytes = wl.algorithmic_bytes({k: v for k, v in inputs.items() if not k.startswith("_")},
+                                                   n_out)
+        algo = in_bytes + (out_bytes if name == "wcoj_materialize" else 0)
+        peak, src = measured_peaks()
+        achieved = algo / per_launch / 1e9
+        roofline = {
+            "bound": "hbm",
+            "kernel": name,
+            "achieved": round(achieved, 2),
+            "peak": peak,
+            "peak_source": src,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": load_profile_traffic(wl.name),
+            "algorithmic_bytes_per_launch": algo,
+            "launch_ms": round(per_launch * 1e3, 3),
+            "launches_per_step": len(kern[name]) / args.steps,
+            "kernel_share_of_step": round(sum(kern[name]) / sum(times), 4),
+            "all_kernels_ms_per_step": {k: round(sum(v) / args.steps * 1e3, 3) for k, v in kern.items()},
+        }
+    result = {
+        "metric": "derived tuples/sec (fixpoint)",
+        "value": tot_out / step_s,
+        "unit": "tuples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3,
+        "fixpoint_wall_s": step_s,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded generator on the device)",
+        "config": dict(wl.config, derived_tuples=tot_out, l2="flushed between steps (512 MiB write)",
+                       parallelism=f"hash-partitioned root keys x{world}" if world > 1 else "single GPU"),
+        "e2e": {
+            "value": tot_out / e2e_s,
+            "unit": "tuples/s",
+            "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": n_out * 4 * (3 if wl.output == "Triangle" else 2),
+            "ms_per_step": e2e_s * 1e3,
+        },
+        "gpu_launches": int(launches / args.steps),
+        "clocks": clocks.summary(),
+        "roofline": roofline,
+    }
+    return result, wl, inputs
+
+
+def make_workload(args, rank, world):
+    cls = WORKLOADS[args.workload]
+    if args.workload == "triangle":
+        return cls(scale=args.scale or 20, edges=args.edges or 16_000_000, rank=rank, world=world)
+    return cls(rank=rank, world=world)
+
+
+# --------------------------------------------------------------------------
+# CPU side: the oracle restatement on a bounded sample
+
+
+def cpu_sample(wl, inputs_host, target_s=12.0, seed=0):
+    """Time the numpy generic join (oracle port of the reference algorithm)
+    on a growing random subset of root keys until ~target_s of work."""
+    from oracle.gj import join_rule
+    from paper_2604_20073_b200 import parse
+
+    prog = parse(wl.program)
+    rule = prog.rules[-1]
+    rels = {k: v for k, v in inputs_host.items()}
+    # pre-sort each atom's relation in its column order (not timed)
+    cache = {}
+
+    def relation_of(pos):
+        atom = rule.body[pos]
+        return rels[atom.relation]
+
+    roots = np.unique(rels[rule.body[0].relation][:, 0])
+    rng = np.random.default_rng(seed)
+    rng.shuffle(roots)
+    take = max(1, len(roots) // 2000)
+    # build the per-atom sorted indexes once, outside the timed region
+    join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=roots[:1], cache=cache)
+    while True:
+        sample = np.sort(roots[:take])
+        t0 = time.perf_counter()
+        out = join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=sample, cache=cache)
+        dt = time.perf_counter() - t0
+        if dt > target_s / 4 or take >= len(roots):
+            return len(out), dt, take, len(roots)
+        take = min(len(roots), int(take * max(2.0, target_s / max(dt, 1e-3) / 2)))
+
+
+def bench_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference CPU algorithm."""
+    import torch
+
+    if rank != 0:
+        return None
+    wl = make_workload(args, 0, 1)
+    torch.cuda.set_device(0) if torch.cuda.is_available() else None
+    inputs = {k: v.cpu().numpy().astype(np.int64).T for k, v in wl.generate().items()}
+    rates = []
+    n = dt = take = nroots = 0
+    for i in range(args.warmup + args.steps):
+        n, dt, take, nroots = cpu_sample(wl, inputs, target_s=8.0, seed=i)
+        if i >= args.warmup:
+            rates.append(n / dt)
+    value = sum(rates) / len(rates)
+    sample = f"{take}/{nroots} random root keys per step (generic join over the sample)"
+    return {
+        "impl": "reference",
+        "metric": "derived tuples/sec (fixpoint)",
+        "value": value,
+        "unit": "tuples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dt * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic (seeded generator)",
+        "config": wl.config,
+        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="triangle")
+    ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (testing)")
+    ap.add_argument("--edges", type=int, default=None, help="R-MAT edge count override (testing)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    dist = None
+    if args.impl == "ours" and world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group("nccl")
+        dist = tdist
+
+    if args.impl == "reference":
+        line = bench_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line))
+        return
+
+    result, wl, inputs = bench_ours(args, rank, world, dist)
+    if rank == 0 and not args.no_cpu_baseline:
+        host = {k: v.cpu().numpy().astype(np.int64).T for k, v in inputs.items() if not k.startswith("_")}
+        n, dt, take, nroots = cpu_sample(wl, host)
+        result["cpu_baseline"] = {
+            "value": n / dt,
+            "unit": "tuples/s",
+            "cores": 1,
+            "kind": "port",
+            "sample": f"{take}/{nroots} random root keys, {n} derived tuples in {dt:.2f} s "
+                      "(numpy generic-join restatement of the reference executor)",
+        }
+    if dist:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+if __name__ == "__main__":
+    main()

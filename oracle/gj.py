@@ -111,13 +111,14 @@ def variable_order(rule, delta_pos=None) -> list:
     return order
 
 
-def join_rule(rule, relation_of, const_id, delta_pos=None, level0_keep=None) -> np.ndarray:
+def join_rule(rule, relation_of, const_id, delta_pos=None, level0_keep=None, cache=None) -> np.ndarray:
     """All head tuples (with duplicates) of one rule instance.
 
     relation_of(body_pos) -> sorted unique int64 rows of that atom's
     relation version; const_id(literal) -> id or None (unknown constant).
     level0_keep optionally restricts the first variable to a sorted set of
-    values (used for bounded samples of large instances).
+    values (used for bounded samples of large instances); `cache` (a dict)
+    keeps each atom's sorted index between calls on unchanged relations.
     """
     order = variable_order(rule, delta_pos)
     level_of = {v: i for i, v in enumerate(order)}
@@ -131,8 +132,13 @@ def join_rule(rule, relation_of, const_id, delta_pos=None, level0_keep=None) -> 
         )
         free = [k for k, t in enumerate(atom.args) if t.kind == VAR and t.value not in level_of]
         perm = consts + bound + free
-        rows = relation_of(pos)
-        rows = sort_dedup(rows[:, perm]) if len(rows) else np.empty((0, atom.arity), np.int64)
+        if cache is not None and pos in cache:
+            rows = cache[pos]
+        else:
+            rows = relation_of(pos)
+            rows = sort_dedup(rows[:, perm]) if len(rows) else np.empty((0, atom.arity), np.int64)
+            if cache is not None:
+                cache[pos] = rows
         lo, hi = 0, len(rows)
         for c, k in enumerate(consts):
             ident = const_id(atom.args[k].value)

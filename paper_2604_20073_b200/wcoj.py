@@ -35,6 +35,22 @@ from .syntax import VAR
 
 WARPS_PER_SM = 28  # 7 resident CTAs x 4 warps (30 KB shared memory each)
 
+# Benchmark hook: when a list, every count/materialize launch appends
+# (name, start_event, end_event) recorded on the launching stream.
+KERNEL_EVENTS = None
+
+
+def _timed(name, fn):
+    if KERNEL_EVENTS is None:
+        return fn()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = fn()
+    b.record()
+    KERNEL_EVENTS.append((name, a, b))
+    return rc
+
 
 def device_warps(p: int = 1) -> int:
     return max(int(p), dev.sm_count() * WARPS_PER_SM)
@@ -286,7 +302,8 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
     )
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
-    dev.check(dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x), dev.stream_handle()), "wcoj_count")
+    dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x),
+                                                                      dev.stream_handle())), "wcoj_count")
     return counts
 
 
@@ -309,8 +326,8 @@ def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep
         error = torch.zeros(1, dtype=torch.int32, device=dev.device())
     desc = prep.descriptor()
     x = _exec_desc(partition, counts, out_cols, error, bitmap)
-    dev.check(dev.lib().srdl_wcoj_materialize(C.byref(desc), C.byref(x), dev.stream_handle()),
-              "wcoj_materialize")
+    dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
+        C.byref(desc), C.byref(x), dev.stream_handle())), "wcoj_materialize")
     if own_flag and int(error.item()):
         raise InternalError(f"plan {plan.plan_id}: materialized tuple count diverged from the count pass")
     return out_cols
