@@ -103,9 +103,8 @@ class TriangleRMAT(Workload):
 
         from paper_2604_20073_b200 import device as dev
 
-        raw = dev.gen_rmat(self.scale, self.nedges, seed=self.seed)
-        keep = raw[0].view(torch.int32) != raw[1].view(torch.int32)
-        raw = raw[:, keep].contiguous()
+        raw = dev.gen_rmat(self.scale, self.nedges, seed=self.seed).view(torch.int32)
+        raw = raw[:, raw[0] != raw[1]].contiguous().view(torch.uint32)  # drop self loops
         return dev.sort_dedup(raw, self.scale)
 
     def generate(self):
@@ -117,9 +116,10 @@ class TriangleRMAT(Workload):
             return {"R": e, "S": e, "T": e}
         # hash partition on the root variable x: R(x, y) by column 0, T(z, x) by column 1
         w = self.world
-        mine_r = (e[0].view(torch.int32) % w) == self.rank
-        mine_t = (e[1].view(torch.int32) % w) == self.rank
-        return {"R": e[:, mine_r].contiguous(), "S": e, "T": e[:, mine_t].contiguous()}
+        ei = e.view(torch.int32)
+        r = ei[:, (ei[0] % w) == self.rank].contiguous().view(torch.uint32)
+        t = ei[:, (ei[1] % w) == self.rank].contiguous().view(torch.uint32)
+        return {"R": r, "S": e, "T": t}
 
     def algorithmic_bytes(self, inputs, n_out):
         # each WCOJ launch must read the three sorted edge indexes once
@@ -155,9 +155,6 @@ class TCRandom(Workload):
         e = torch.from_numpy(np.array([src, dst], dtype=np.uint32)).to(dev.device())
         e = dev.sort_dedup(e, 32)
         self.config["edges"] = int(e.shape[1])
-        if self.world > 1:
-            mine = (e[0].view(torch.int32) % self.world) == self.rank
-            return {"Edge": e, "_shard": e[:, mine]}
         return {"Edge": e}
 
     def algorithmic_bytes(self, inputs, n_out):

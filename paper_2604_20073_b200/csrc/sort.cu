@@ -247,11 +247,28 @@ __global__ void gather_cols(Cols cols, uint32_t arity, const uint32_t *__restric
     }
 }
 
-__global__ void check_sorted(Cols rows, uint64_t n, uint32_t arity, int *bad) {
+// bad = 1 if some row is greater than (strict: not less than) its successor
+__global__ void check_sorted(Cols rows, uint64_t n, uint32_t arity, int strict, int *bad) {
+    const int limit = strict ? 0 : 1;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        if (row_cmp(rows, i, rows, i + 1, arity) >= 0) atomicExch(bad, 1);
+        if (row_cmp(rows, i, rows, i + 1, arity) >= limit) {
+            atomicExch(bad, 1);
+            return;
+        }
     }
+}
+
+static bool rows_sorted(const Cols &rows, uint64_t n, uint32_t arity, bool strict, cudaStream_t s) {
+    if (n <= 1) return true;
+    Scratch bad(sizeof(int), s);
+    SRDL_CUDA(cudaMemsetAsync(bad.as<int>(), 0, sizeof(int), s));
+    check_sorted<<<stride_grid(n), kThreads, 0, s>>>(rows, n, arity, strict ? 1 : 0, bad.as<int>());
+    SRDL_CHECK_LAUNCH();
+    int h = 0;
+    SRDL_CUDA(cudaMemcpyAsync(&h, bad.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    SRDL_CUDA(cudaStreamSynchronize(s));
+    return h == 0;
 }
 
 // Sort + unique + anti-join; the heart of compute_delta.
@@ -270,7 +287,16 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
     Scratch keep(n * sizeof(uint32_t), s);
     Scratch total(sizeof(uint32_t) * 2, s);
     const uint32_t per_chunk = 64 / bits;
-    if (arity <= per_chunk) {
+    if (rows_sorted(in, n, arity, false, s)) {
+        // staged rows already in index order (e.g. WCOJ output enumerated in
+        // variable order): unique + anti-join without sorting
+        flag_rows<<<g, kThreads, 0, s>>>(in, n, S, arity, keep.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        Scratch pos(n * sizeof(uint32_t), s);
+        exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
+        scatter_rows<<<g, kThreads, 0, s>>>(in, keep.as<uint32_t>(), pos.as<uint32_t>(), n, arity, dst);
+        SRDL_CHECK_LAUNCH();
+    } else if (arity <= per_chunk) {
         pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, arity}, bits, nullptr, n, keys.as<uint64_t>());
         SRDL_CHECK_LAUNCH();
         radix_sort(keys.as<uint64_t>(), nullptr, n, arity * bits, s);
@@ -358,15 +384,7 @@ int srdl_is_sorted_strict(const uint32_t *const *cols, uint32_t arity, uint64_t 
         cudaStream_t s = (cudaStream_t)stream;
         *ok = 1;
         if (n <= 1) return;
-        Scratch bad(sizeof(int), s);
-        SRDL_CUDA(cudaMemsetAsync(bad.as<int>(), 0, sizeof(int), s));
-        check_sorted<<<stride_grid(n), kThreads, 0, s>>>(make_cols(cols, arity), n, arity,
-                                                        bad.as<int>());
-        SRDL_CHECK_LAUNCH();
-        int h = 0;
-        SRDL_CUDA(cudaMemcpyAsync(&h, bad.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, s));
-        SRDL_CUDA(cudaStreamSynchronize(s));
-        *ok = !h;
+        *ok = rows_sorted(make_cols(cols, arity), n, arity, true, s) ? 1 : 0;
     });
 }
 
