@@ -138,34 +138,45 @@ typedef struct {
 /* at most this many atoms may constrain the last variable of a plan */
 #define SRDL_MAX_LEAF_SPECS 6
 
-/* Root work space of one plan execution (Alg. 1 phase 1, Fig. 2). */
+/* Root work space of one plan execution (Alg. 1 phase 1, Fig. 2).
+ * The flattened units [0, T) are cut into `nslices` equal slices; launched
+ * warps fetch slice indexes from `ticket` (one atomic per slice), so the
+ * output offsets depend only on the slice, never on which warp ran it. */
 typedef struct {
     const uint32_t *keys;    /* K root keys (outer histogram keys)            */
     const uint32_t *d2;      /* K inner degrees (1 without inner source)      */
     const uint64_t *prefix;  /* K inclusive prefix of outer_degree * d2       */
+    const uint32_t *outer_deg; /* K outer degrees                             */
+    const uint32_t *outer_lo;  /* K first outer row of each key, or NULL       */
+    const uint32_t *inner_lo;  /* K first inner row of each key, or NULL       */
     uint64_t nkeys;
-    uint32_t nwarps;         /* slices p; warp w owns [w*ceil(T/p), ...)      */
-    uint64_t *warp_counts;   /* p: tuples counted per slice                   */
-    uint64_t *warp_offsets;  /* p: exclusive prefix of warp_counts            */
-    uint64_t *total;         /* device scalar: sum of warp_counts             */
+    uint32_t nwarps;         /* warps launched                                */
+    uint32_t nslices;        /* slices of [0, T)                              */
+    uint32_t *ticket;        /* device counter, zero before each launch       */
+    uint64_t *slice_counts;  /* nslices: tuples counted per slice             */
+    uint64_t *slice_offsets; /* nslices: exclusive prefix of slice_counts     */
+    uint64_t *total;         /* device scalar: sum of slice_counts            */
     uint32_t *out[SRDL_MAX_HEAD];
     uint32_t *error;         /* device flag, non-zero on count/write mismatch */
     uint32_t *bitmap;        /* optional (audit): per-output-slot write counter */
 } srdl_exec;
 
 /* reference: executor.build_partition (executor.py:246). From the outer
- * histogram (keys, degrees) and the inner histogram (may be empty), write
- * d2[K] and the inclusive work prefix[K] (uint64). No host sync. */
-int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, uint64_t nk, const uint32_t *ikeys,
-                   const uint32_t *ideg, uint64_t nik, int has_inner, uint32_t *d2,
-                   uint64_t *prefix, void *stream);
+ * histogram (keys, degrees, inclusive prefix) and the inner histogram (may be
+ * empty), write d2[K], the inclusive work prefix[K] (uint64) and, when the
+ * row-start arrays are given, the first outer / inner row of every key
+ * (outer_lo = oprefix - odeg; inner_lo = iprefix - ideg of the same key). */
+int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, const uint64_t *oprefix,
+                   uint64_t nk, const uint32_t *ikeys, const uint32_t *ideg,
+                   const uint64_t *iprefix, uint64_t nik, int has_inner, uint32_t *d2,
+                   uint64_t *prefix, uint32_t *outer_lo, uint32_t *inner_lo, void *stream);
 
 /* reference: executor.count_pass (executor.py:439). Count kernel over the
- * flattened slices + exclusive scan into warp_offsets/total. No host sync. */
+ * flattened slices + exclusive scan into slice_offsets/total. No host sync. */
 int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream);
 
 /* reference: executor.materialize_pass (executor.py:458). Re-walks the
- * slices writing head tuples at warp_offsets; sets *error on divergence. */
+ * slices writing head tuples at slice_offsets; sets *error on divergence. */
 int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stream);
 
 /* ------------------------------------------------------------- generators

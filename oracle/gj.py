@@ -87,7 +87,7 @@ def _narrow(col, lo, hi, v):
 
 
 class _Src:
-    __slots__ = ("rows", "negated", "col_levels", "nconst", "levels")
+    __slots__ = ("rows", "negated", "col_levels", "nconst", "levels", "bits", "_keys")
 
     def __init__(self, rows, negated, col_levels, nconst):
         self.rows = rows
@@ -97,6 +97,34 @@ class _Src:
         self.levels: dict = {}
         for off, lvl in enumerate(col_levels):
             self.levels.setdefault(lvl, []).append(nconst + off)
+        top = int(rows.max()) if rows.size else 0
+        self.bits = max(1, top.bit_length())
+        self._keys: dict = {}
+
+    def prefix_keys(self, c):
+        """Sorted packed keys of columns 0..c (None when they do not fit)."""
+        if (c + 1) * self.bits > 62:
+            return None
+        k = self._keys.get(c)
+        if k is None:
+            k = self.rows[:, 0].copy() if c == 0 else (self.prefix_keys(c - 1) << self.bits) | self.rows[:, c]
+            self._keys[c] = k
+        return k
+
+    def narrow(self, c, lo, hi, v):
+        """Rows of [lo, hi) (all sharing columns < c) whose column c equals v."""
+        keys = self.prefix_keys(c)
+        if keys is None or np.any(v >= (1 << self.bits)):
+            return _narrow(self.rows[:, c], lo, hi, v)
+        nonempty = lo < hi
+        if c == 0:
+            q = v
+        else:
+            base = self.prefix_keys(c - 1)[np.minimum(lo, len(self.rows) - 1)]
+            q = (base << self.bits) | v
+        a = np.searchsorted(keys, q, "left")
+        b = np.searchsorted(keys, q, "right")
+        return np.where(nonempty, a, lo), np.where(nonempty, b, lo)
 
 
 def variable_order(rule, delta_pos=None) -> list:
@@ -192,7 +220,7 @@ def join_rule(rule, relation_of, const_id, delta_pos=None, level0_keep=None, cac
             s = srcs[a][0]
             lo, hi = new_lo[a], new_hi[a]
             for c in cols:
-                lo, hi = _narrow(s.rows[:, c], lo, hi, v)
+                lo, hi = s.narrow(c, lo, hi, v)
             new_lo[a], new_hi[a] = lo, hi
             if not s.negated:
                 alive &= lo < hi

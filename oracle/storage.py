@@ -23,10 +23,42 @@ def lex_order(rows: np.ndarray) -> np.ndarray:
     return np.lexsort(rows.T[::-1])
 
 
+def _packable(*arrays):
+    """Bit width per column if every row of every array packs into 63 bits."""
+    arity = arrays[0].shape[1]
+    top = 0
+    for a in arrays:
+        if a.size:
+            if a.min() < 0:
+                return None
+            top = max(top, int(a.max()))
+    bits = max(1, top.bit_length())
+    return bits if bits * arity <= 63 else None
+
+
+def _pack(rows: np.ndarray, bits: int) -> np.ndarray:
+    key = np.zeros(len(rows), np.int64)
+    for k in range(rows.shape[1]):
+        key = (key << bits) | rows[:, k]
+    return key
+
+
+def _unpack(keys: np.ndarray, bits: int, arity: int) -> np.ndarray:
+    out = np.empty((len(keys), arity), np.int64)
+    mask = (1 << bits) - 1
+    for k in range(arity - 1, -1, -1):
+        out[:, k] = keys & mask
+        keys = keys >> bits
+    return out
+
+
 def sort_dedup(rows: np.ndarray) -> np.ndarray:
     """Sorted distinct rows (reference rowops.sort_dedup, :60)."""
     if len(rows) <= 1:
         return rows.copy()
+    bits = _packable(rows)
+    if bits is not None and rows.shape[1] > 0:
+        return _unpack(np.unique(_pack(rows, bits)), bits, rows.shape[1])
     s = rows[lex_order(rows)]
     keep = np.ones(len(s), bool)
     keep[1:] = np.any(s[1:] != s[:-1], axis=1)
@@ -65,6 +97,11 @@ def member(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """Per-row membership of a in b (reference rowops.member_mask, :95)."""
     if len(a) == 0 or len(b) == 0:
         return np.zeros(len(a), bool)
+    bits = _packable(a, b) if a.shape[1] else None
+    if bits is not None:
+        ka, kb = _pack(a, bits), np.sort(_pack(b, bits))
+        pos = np.minimum(np.searchsorted(kb, ka), len(kb) - 1)
+        return kb[pos] == ka
     ka, kb = _row_keys(a, b)
     return np.isin(ka, kb)
 

@@ -110,12 +110,14 @@ __global__ void combine_pairs(const uint32_t *__restrict__ mk, const uint32_t *_
 }
 
 __global__ void root_work_kernel(const uint32_t *__restrict__ okeys, const uint32_t *__restrict__ odeg,
-                                 uint64_t nk, const uint32_t *__restrict__ ikeys,
-                                 const uint32_t *__restrict__ ideg, uint64_t nik, int has_inner,
-                                 uint32_t *__restrict__ d2, uint64_t *__restrict__ work) {
+                                 const uint64_t *__restrict__ oprefix, uint64_t nk,
+                                 const uint32_t *__restrict__ ikeys, const uint32_t *__restrict__ ideg,
+                                 const uint64_t *__restrict__ iprefix, uint64_t nik, int has_inner,
+                                 uint32_t *__restrict__ d2, uint64_t *__restrict__ work,
+                                 uint32_t *__restrict__ outer_lo, uint32_t *__restrict__ inner_lo) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t d = 1;
+        uint32_t d = 1, ilo = 0;
         if (has_inner) {
             uint32_t k = okeys[i];
             uint64_t lo = 0, hi = nik;
@@ -123,10 +125,14 @@ __global__ void root_work_kernel(const uint32_t *__restrict__ okeys, const uint3
                 uint64_t m = (lo + hi) >> 1;
                 if (ikeys[m] < k) lo = m + 1; else hi = m;
             }
-            d = (lo < nik && ikeys[lo] == k) ? ideg[lo] : 0u;
+            const bool found = lo < nik && ikeys[lo] == k;
+            d = found ? ideg[lo] : 0u;
+            if (found && iprefix) ilo = (uint32_t)(iprefix[lo] - ideg[lo]);
         }
         d2[i] = d;
         work[i] = (uint64_t)odeg[i] * d;
+        if (outer_lo) outer_lo[i] = (uint32_t)(oprefix[i] - odeg[i]);
+        if (inner_lo) inner_lo[i] = ilo;
     }
 }
 
@@ -282,14 +288,18 @@ int srdl_narrow_prefix(const uint32_t *const *cols, uint64_t n, const uint32_t *
     });
 }
 
-int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, uint64_t nk, const uint32_t *ikeys,
-                   const uint32_t *ideg, uint64_t nik, int has_inner, uint32_t *d2,
-                   uint64_t *prefix, void *stream) {
+int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, const uint64_t *oprefix,
+                   uint64_t nk, const uint32_t *ikeys, const uint32_t *ideg,
+                   const uint64_t *iprefix, uint64_t nik, int has_inner, uint32_t *d2,
+                   uint64_t *prefix, uint32_t *outer_lo, uint32_t *inner_lo, void *stream) {
     return guarded([&] {
         if (nk == 0) return;
+        SRDL_REQUIRE(!outer_lo || oprefix, "outer_lo needs the outer prefix");
+        SRDL_REQUIRE(!inner_lo || iprefix, "inner_lo needs the inner prefix");
         cudaStream_t s = (cudaStream_t)stream;
-        root_work_kernel<<<stride_grid(nk), kThreads, 0, s>>>(okeys, odeg, nk, ikeys, ideg, nik,
-                                                              has_inner, d2, prefix);
+        root_work_kernel<<<stride_grid(nk), kThreads, 0, s>>>(okeys, odeg, oprefix, nk, ikeys, ideg,
+                                                              iprefix, nik, has_inner, d2, prefix,
+                                                              outer_lo, inner_lo);
         SRDL_CHECK_LAUNCH();
         inclusive_scan_u64(prefix, prefix, nk, s);
     });

@@ -3,10 +3,14 @@
 // _run_slice / _root_setup / _descend, executor.py:342-485).
 //
 // Work decomposition. The root level is flattened into T = sum_k outer(k) *
-// d2(k) units (prefix array C). Warp w owns units [w*ceil(T/p), (w+1)*ceil(T/p)),
-// finds its first key by binary search on C (kappa) and walks its slice as
-// at most three (outer rows x inner rows) rectangles per key, exactly the
-// Fig. 2 scheme, so a heavy root key is spread over many warps.
+// d2(k) units (prefix array C) and cut into p equal slices [s*ceil(T/p), ...)
+// (Alg. 2 "block b's slice"); p is many times the number of resident warps
+// and warps fetch slice indexes from a ticket counter, so cost variance
+// between slices (light keys carry per-key overhead the unit count does not
+// see) evens out. A slice finds its first key by binary search on C (kappa)
+// and is walked as at most three (outer rows x inner rows) rectangles per
+// key, exactly the Fig. 2 scheme. Output offsets are per slice, so results
+// do not depend on which warp ran which slice.
 //
 // Inside a rectangle the warp runs leapfrog-style generic join over the
 // remaining levels with all 32 lanes cooperating:
@@ -28,6 +32,8 @@ namespace srdl {
 
 constexpr int kJoinWarps = 4;
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr uint32_t kMergeMin = 64;    // shortest list length for merge-path leaves
+constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge-path
 
 struct Rng {
     uint32_t lo, hi;
@@ -124,6 +130,47 @@ struct Sink {
     }
 };
 
+// Warp-cooperative merge-path intersection of two single-segment sorted
+// leaf lists (both positive, one column each): tiles of 32 values from both
+// lists are loaded coalesced, each lane locates its A value in the B tile
+// with a 5-step shuffle search, and the tiles advance past
+// min(last A, last B). Used for "heavy" parents whose lists are long and of
+// comparable length, where per-element binary search would cost
+// min(a,b)*log(max(a,b)) dependent loads against (a+b)/32 coalesced steps.
+template <bool WRITE>
+__device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const WarpState &S, uint32_t p,
+                           Sink<WRITE> &sink) {
+    const int leaf = (int)P.depth - 1;
+    const uint32_t ja = S.leaf_drv[p], jb = 1u - ja;
+    const srdl_atom &A = P.atom[P.spec[leaf][ja]];
+    const srdl_atom &B = P.atom[P.spec[leaf][jb]];
+    const uint32_t *ca = A.seg[0].cols[A.lvl_col[leaf]];
+    const uint32_t *cb = B.seg[0].cols[B.lvl_col[leaf]];
+    uint32_t ia = S.leaf[p][ja][0].lo, ea = S.leaf[p][ja][0].hi;
+    uint32_t ib = S.leaf[p][jb][0].lo, eb = S.leaf[p][jb][0].hi;
+    const uint32_t l = lane_id();
+    while (ia < ea && ib < eb) {
+        const bool va = ia + l < ea, vb = ib + l < eb;
+        const uint32_t av = va ? __ldg(ca + ia + l) : 0xffffffffu;
+        const uint32_t bv = vb ? __ldg(cb + ib + l) : 0xffffffffu;
+        const uint32_t na_tile = min(32u, ea - ia), nb_tile = min(32u, eb - ib);
+        const uint32_t alast = __shfl_sync(kFull, av, na_tile - 1);
+        const uint32_t blast = __shfl_sync(kFull, bv, nb_tile - 1);
+        const uint32_t m = min(alast, blast);
+        uint32_t cnt = 0;  // B tile values < av
+#pragma unroll
+        for (uint32_t st = 16; st; st >>= 1) {
+            const uint32_t probe = __shfl_sync(kFull, bv, cnt + st - 1);
+            if (probe < av) cnt += st;
+        }
+        const uint32_t hit = __shfl_sync(kFull, bv, cnt);
+        const bool take_a = va && av <= m;
+        sink.emit(P, X, S, take_a && hit == av, p, av, leaf);
+        ia += __popc(__ballot_sync(kFull, take_a));
+        ib += __popc(__ballot_sync(kFull, vb && bv <= m));
+    }
+}
+
 // Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
 // level m-2 chunk; for m == 2 the single parent is the root rectangle).
 template <bool WRITE>
@@ -132,9 +179,17 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
     const int leaf = (int)P.depth - 1;
     const uint32_t nls = P.nspec[leaf];
     const uint32_t l = lane_id();
+    // two plain positive sources on the leaf variable: merge-path candidates
+    bool pairable = nls == 2;
+    if (pairable) {
+        const srdl_atom &A0 = P.atom[P.spec[leaf][0]];
+        const srdl_atom &A1 = P.atom[P.spec[leaf][1]];
+        pairable = !A0.negated && !A1.negated && A0.lvl_ncol[leaf] == 1 && A1.lvl_ncol[leaf] == 1;
+    }
     uint64_t len = 0;
+    bool heavy = false;
     if ((parents >> l) & 1u) {
-        uint32_t best = 0xffffffffu, bj = 0;
+        uint32_t best = 0xffffffffu, bj = 0, worst = 0;
         for (uint32_t j = 0; j < nls; ++j) {
             const srdl_atom &A = P.atom[P.spec[leaf][j]];
             if (A.negated) continue;
@@ -144,10 +199,21 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
                 best = t;
                 bj = j;
             }
+            worst = t > worst ? t : worst;
         }
         len = best;
         S.leaf_drv[l] = (uint8_t)bj;
+        if (pairable && best >= kMergeMin && worst <= best * kMergeRatio) {
+            const Rng a1 = S.leaf[l][0][1], b1 = S.leaf[l][1][1];
+            const bool single = (P.atom[P.spec[leaf][0]].nseg < 2 || a1.lo >= a1.hi) &&
+                                (P.atom[P.spec[leaf][1]].nseg < 2 || b1.lo >= b1.hi);
+            if (single) {
+                heavy = true;
+                len = 0;  // handled by merge_pair below
+            }
+        }
     }
+    const uint32_t heavy_mask = __ballot_sync(kFull, heavy);
     uint64_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -210,6 +276,7 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
         sink.emit(P, X, S, alive, p, v, leaf);
     }
     __syncwarp();
+    for (uint32_t hm = heavy_mask; hm; hm &= hm - 1) merge_pair<WRITE>(P, X, S, __ffs(hm) - 1, sink);
 }
 
 // Pick the smallest candidate source of level L and reset the chunk cursor.
@@ -317,8 +384,9 @@ __device__ __forceinline__ void descend(const srdl_plan &P, WarpState &S, int L,
 
 // One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
 template <bool WRITE>
-__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t key,
-                         uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1, Sink<WRITE> &sink) {
+__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint64_t k,
+                         uint32_t key, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
+                         Sink<WRITE> &sink) {
     const uint32_t l = lane_id();
     const uint32_t a = l / SRDL_MAX_SEGS, s = l % SRDL_MAX_SEGS;
     const bool mine = a < P.natoms;
@@ -331,10 +399,18 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, u
     }
     if (mine) has0 = A.lvl_ncol[0] != 0;
     if (has0 && lo < hi) {
-        Rng t{lo, hi};
-        narrow_first(A, s, 0, key, t);
-        lo = t.lo;
-        hi = t.hi;
+        if (a == P.outer && X.outer_lo) {  // single segment: rows straight from the histogram
+            lo += X.outer_lo[k];
+            hi = lo + X.outer_deg[k];
+        } else if (a == P.inner && X.inner_lo) {
+            lo += X.inner_lo[k];
+            hi = lo + X.d2[k];
+        } else {
+            Rng t{lo, hi};
+            narrow_first(A, s, 0, key, t);
+            lo = t.lo;
+            hi = t.hi;
+        }
     }
     const uint32_t n_here = hi - lo;
     const uint32_t n0 = __shfl_sync(kFull, n_here, l & ~1u);
@@ -413,54 +489,60 @@ __global__ void __launch_bounds__(kJoinWarps * 32)
     wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X) {
     __shared__ WarpState states[kJoinWarps];
     const uint32_t wib = threadIdx.x >> 5;
-    const uint32_t w = blockIdx.x * kJoinWarps + wib;
-    if (w >= X.nwarps) return;
     WarpState &S = states[wib];
     const uint64_t K = X.nkeys;
     const uint64_t T = K ? X.prefix[K - 1] : 0;
-    const uint64_t step = (T + X.nwarps - 1) / X.nwarps;
-    uint64_t bs = (uint64_t)w * step, be = bs + step;
-    if (bs > T) bs = T;
-    if (be > T) be = T;
-    Sink<WRITE> sink{0, WRITE ? X.warp_offsets[w] : 0};
-    if (bs < be) {
-        // kappa: first key whose inclusive prefix exceeds bs
-        uint64_t lo = 0, hi = K;
-        while (lo < hi) {
-            uint64_t mid = (lo + hi) >> 1;
-            if (X.prefix[mid] <= bs)
-                lo = mid + 1;
-            else
-                hi = mid;
-        }
-        for (uint64_t k = lo; k < K; ++k) {
-            const uint64_t start = k ? X.prefix[k - 1] : 0;
-            if (start >= be) break;
-            const uint64_t end = X.prefix[k];
-            const uint64_t u0 = (bs > start ? bs : start) - start;
-            const uint64_t u1 = (be < end ? be : end) - start;
-            if (u0 >= u1) continue;
-            const uint64_t d2 = X.d2[k];
-            const uint32_t key = X.keys[k];
-            uint64_t ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
-            if (ra == rb) {
-                run_rect<WRITE>(P, X, S, key, ra, ra + 1, ca, cb, sink);
-                continue;
+    const uint64_t step = (T + X.nslices - 1) / X.nslices;
+    while (true) {
+        // dynamic slice fetch: any warp may run any slice, offsets are per slice
+        uint32_t sl = 0;
+        if (lane_id() == 0) sl = atomicAdd(X.ticket, 1u);
+        sl = __shfl_sync(kFull, sl, 0);
+        if (sl >= X.nslices) break;
+        uint64_t bs = (uint64_t)sl * step, be = bs + step;
+        if (bs > T) bs = T;
+        if (be > T) be = T;
+        Sink<WRITE> sink{0, WRITE ? X.slice_offsets[sl] : 0};
+        if (bs < be) {
+            // kappa: first key whose inclusive prefix exceeds bs
+            uint64_t lo = 0, hi = K;
+            while (lo < hi) {
+                uint64_t mid = (lo + hi) >> 1;
+                if (X.prefix[mid] <= bs)
+                    lo = mid + 1;
+                else
+                    hi = mid;
             }
-            if (ca) {
-                run_rect<WRITE>(P, X, S, key, ra, ra + 1, ca, d2, sink);
-                ++ra;
+            for (uint64_t k = lo; k < K; ++k) {
+                const uint64_t start = k ? X.prefix[k - 1] : 0;
+                if (start >= be) break;
+                const uint64_t end = X.prefix[k];
+                const uint64_t u0 = (bs > start ? bs : start) - start;
+                const uint64_t u1 = (be < end ? be : end) - start;
+                if (u0 >= u1) continue;
+                const uint64_t d2 = X.d2[k];
+                const uint32_t key = X.keys[k];
+                uint64_t ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
+                if (ra == rb) {
+                    run_rect<WRITE>(P, X, S, k, key, ra, ra + 1, ca, cb, sink);
+                    continue;
+                }
+                if (ca) {
+                    run_rect<WRITE>(P, X, S, k, key, ra, ra + 1, ca, d2, sink);
+                    ++ra;
+                }
+                if (ra < rb) run_rect<WRITE>(P, X, S, k, key, ra, rb, 0, d2, sink);
+                if (cb) run_rect<WRITE>(P, X, S, k, key, rb, rb + 1, 0, cb, sink);
             }
-            if (ra < rb) run_rect<WRITE>(P, X, S, key, ra, rb, 0, d2, sink);
-            if (cb) run_rect<WRITE>(P, X, S, key, rb, rb + 1, 0, cb, sink);
         }
-    }
-    if (lane_id() == 0) {
-        if (WRITE) {
-            if (sink.n != X.warp_counts[w]) atomicExch(X.error, 1u);
-        } else {
-            X.warp_counts[w] = sink.n;
+        if (lane_id() == 0) {
+            if (WRITE) {
+                if (sink.n != X.slice_counts[sl]) atomicExch(X.error, 1u);
+            } else {
+                X.slice_counts[sl] = sink.n;
+            }
         }
+        __syncwarp();
     }
 }
 
@@ -470,7 +552,8 @@ static void check_plan(const srdl_plan *P, const srdl_exec *X) {
     SRDL_REQUIRE(P->head_arity <= SRDL_MAX_HEAD, "head arity %u", P->head_arity);
     SRDL_REQUIRE(P->nspec[P->depth - 1] <= SRDL_MAX_LEAF_SPECS, "leaf level has %u sources (max %d)",
                  P->nspec[P->depth - 1], SRDL_MAX_LEAF_SPECS);
-    SRDL_REQUIRE(X->nwarps >= 1, "nwarps must be >= 1");
+    SRDL_REQUIRE(X->nwarps >= 1 && X->nslices >= 1, "nwarps and nslices must be >= 1");
+    SRDL_REQUIRE(X->ticket != nullptr, "a slice ticket counter is required");
 }
 
 }  // namespace srdl
@@ -484,9 +567,10 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
         const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
+        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
         wcoj_kernel<false><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
         SRDL_CHECK_LAUNCH();
-        exclusive_scan_u64(ex->warp_counts, ex->warp_offsets, ex->nwarps, ex->total, s);
+        exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
     });
 }
 
@@ -495,6 +579,7 @@ int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stre
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
         const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
+        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
         wcoj_kernel<true><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
         SRDL_CHECK_LAUNCH();
     });

@@ -75,10 +75,15 @@ class ExecDesc(C.Structure):
         ("keys", C.c_void_p),
         ("d2", C.c_void_p),
         ("prefix", C.c_void_p),
+        ("outer_deg", C.c_void_p),
+        ("outer_lo", C.c_void_p),
+        ("inner_lo", C.c_void_p),
         ("nkeys", C.c_uint64),
         ("nwarps", C.c_uint32),
-        ("warp_counts", C.c_void_p),
-        ("warp_offsets", C.c_void_p),
+        ("nslices", C.c_uint32),
+        ("ticket", C.c_void_p),
+        ("slice_counts", C.c_void_p),
+        ("slice_offsets", C.c_void_p),
         ("total", C.c_void_p),
         ("out", C.c_void_p * MAX_HEAD),
         ("error", C.c_void_p),
@@ -127,8 +132,8 @@ _SIGNATURES = {
     ),
     "srdl_root_work": (
         C.c_int,
-        [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int,
-         C.c_void_p, C.c_void_p, C.c_void_p],
+        [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
     "srdl_wcoj_count": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
     "srdl_wcoj_materialize": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
@@ -347,20 +352,31 @@ def narrow_prefix(rows: torch.Tensor, lo: int, hi: int, values) -> tuple:
     return lo + a.value, lo + b.value
 
 
-def root_work(okeys, odeg, ikeys=None, ideg=None):
-    """(d2 u32, inclusive work prefix i64) for an outer/inner histogram pair."""
+def root_work(okeys, odeg, oprefix=None, ikeys=None, ideg=None, iprefix=None, outer_rows=False,
+              inner_rows=False):
+    """Root work space: (d2 u32, inclusive work prefix i64, outer_lo, inner_lo).
+
+    outer_lo / inner_lo (u32 first row of every key) are produced only when
+    requested (single-segment sources); else None."""
     nk = okeys.numel()
-    d2 = torch.empty(nk, dtype=U32, device=device())
-    prefix = torch.empty(nk, dtype=U64, device=device())
+    d = device()
+    d2 = torch.empty(nk, dtype=U32, device=d)
+    prefix = torch.empty(nk, dtype=U64, device=d)
+    olo = torch.empty(nk, dtype=U32, device=d) if outer_rows else None
+    ilo = torch.empty(nk, dtype=U32, device=d) if inner_rows else None
     if nk == 0:
-        return d2, prefix
+        return d2, prefix, olo, ilo
     has_inner = ikeys is not None
-    check(lib().srdl_root_work(okeys.data_ptr(), odeg.data_ptr(), nk,
-                               ikeys.data_ptr() if has_inner and ikeys.numel() else None,
-                               ideg.data_ptr() if has_inner and ideg.numel() else None,
-                               ikeys.numel() if has_inner else 0, int(has_inner), d2.data_ptr(),
-                               prefix.data_ptr(), stream_handle()), "root_work")
-    return d2, prefix
+    nik = ikeys.numel() if has_inner else 0
+
+    def p(t):
+        return t.data_ptr() if t is not None and t.numel() else None
+
+    check(lib().srdl_root_work(okeys.data_ptr(), odeg.data_ptr(), p(oprefix), nk,
+                               p(ikeys) if has_inner else None, p(ideg) if has_inner else None,
+                               p(iprefix) if has_inner else None, nik, int(has_inner), d2.data_ptr(),
+                               prefix.data_ptr(), p(olo), p(ilo), stream_handle()), "root_work")
+    return d2, prefix, olo, ilo
 
 
 def gen_rmat(scale: int, nedges: int, a=0.57, b=0.19, c=0.19, seed=1) -> torch.Tensor:

@@ -34,6 +34,7 @@ from .partition import WorkPartition, decode_workunit, encode_workunit, rectangl
 from .syntax import VAR
 
 WARPS_PER_SM = 28  # 7 resident CTAs x 4 warps (30 KB shared memory each)
+SLICES_PER_WARP = 16  # root slices per launched warp, fetched dynamically
 
 # Benchmark hook: when a list, every count/materialize launch appends
 # (name, start_event, end_event) recorded on the launching stream.
@@ -160,17 +161,23 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
 
 
 class DevicePartition:
-    """Root work space on the device (keys, outer degrees, d2, prefix)."""
+    """Root work space on the device (keys, outer degrees, d2, prefix, and
+    the first outer/inner row of every key when the sources are single
+    segments)."""
 
-    __slots__ = ("keys", "outer_degrees", "d2", "prefix", "p", "nwarps", "_total")
+    __slots__ = ("keys", "outer_degrees", "d2", "prefix", "outer_lo", "inner_lo", "p", "nwarps",
+                 "nslices", "_total")
 
-    def __init__(self, keys, outer_degrees, d2, prefix, p):
+    def __init__(self, keys, outer_degrees, d2, prefix, p, outer_lo=None, inner_lo=None):
         self.keys = keys
         self.outer_degrees = outer_degrees
         self.d2 = d2
         self.prefix = prefix
+        self.outer_lo = outer_lo
+        self.inner_lo = inner_lo
         self.p = p
         self.nwarps = device_warps(p)
+        self.nslices = self.nwarps * SLICES_PER_WARP
         self._total = None
 
     @classmethod
@@ -198,7 +205,7 @@ class DevicePartition:
         )
 
     def slice_sizes(self) -> list:
-        t, n = self.total, self.nwarps
+        t, n = self.total, self.nslices
         step = -(-t // n) if t else 0
         return [max(0, min((w + 1) * step, t) - min(w * step, t)) for w in range(n)]
 
@@ -213,31 +220,34 @@ def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None,
     outer = plan.atoms[plan.outer_atom]
     if outer.n_const == 0:
         hist = prep.rels[plan.outer_atom].hist
-        okeys, odeg = hist.keys, hist.degrees
     else:
         from .columns import Histogram
 
-        h = Histogram.empty()
+        hist = Histogram.empty()
         for rows, lo, hi in prep.segs[plan.outer_atom]:
-            h = h.updated(rows[outer.n_const, lo:hi].contiguous())
-        okeys, odeg = h.keys, h.degrees
+            hist = hist.updated(rows[outer.n_const, lo:hi].contiguous())
+    okeys, odeg = hist.keys, hist.degrees
     if okeys.numel() == 0:
         return DevicePartition.empty(p)
+    single_outer = len(prep.segs[plan.outer_atom]) == 1
     if plan.inner_atom is not None:
         ih = prep.rels[plan.inner_atom].hist
-        d2, prefix = dev.root_work(okeys, odeg, ih.keys, ih.degrees)
+        single_inner = len(prep.segs[plan.inner_atom]) == 1
+        d2, prefix, olo, ilo = dev.root_work(okeys, odeg, hist.prefix, ih.keys, ih.degrees, ih.prefix,
+                                             outer_rows=single_outer, inner_rows=single_inner)
     else:
-        d2, prefix = dev.root_work(okeys, odeg)
-    return DevicePartition(okeys, odeg, d2, prefix, p)
+        d2, prefix, olo, ilo = dev.root_work(okeys, odeg, hist.prefix, outer_rows=single_outer)
+    return DevicePartition(okeys, odeg, d2, prefix, p, olo, ilo)
 
 
 @dataclass
 class CountResult:
     """Per-slice counts (device), their exclusive prefix and the total."""
 
-    warp_counts: torch.Tensor
-    warp_offsets: torch.Tensor
+    slice_counts: torch.Tensor
+    slice_offsets: torch.Tensor
     total_dev: torch.Tensor
+    ticket: torch.Tensor | None = None
     _total: int | None = None
 
     @classmethod
@@ -247,7 +257,7 @@ class CountResult:
         counts[0] = first
         offs = torch.zeros(n_slices, dtype=dev.U64, device=d)
         offs[1:] = first
-        return cls(counts, offs, torch.full((1,), first, dtype=dev.U64, device=d), first)
+        return cls(counts, offs, torch.full((1,), first, dtype=dev.U64, device=d), None, first)
 
     @property
     def total(self) -> int:
@@ -257,11 +267,11 @@ class CountResult:
 
     @property
     def tc(self) -> np.ndarray:
-        return self.warp_counts.cpu().numpy()
+        return self.slice_counts.cpu().numpy()
 
     @property
     def offsets(self) -> np.ndarray:
-        return self.warp_offsets.cpu().numpy()
+        return self.slice_offsets.cpu().numpy()
 
 
 def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=None,
@@ -270,10 +280,15 @@ def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=
     x.keys = partition.keys.data_ptr()
     x.d2 = partition.d2.data_ptr()
     x.prefix = partition.prefix.data_ptr()
+    x.outer_deg = partition.outer_degrees.data_ptr()
+    x.outer_lo = partition.outer_lo.data_ptr() if partition.outer_lo is not None else None
+    x.inner_lo = partition.inner_lo.data_ptr() if partition.inner_lo is not None else None
     x.nkeys = partition.nkeys
     x.nwarps = partition.nwarps
-    x.warp_counts = counts.warp_counts.data_ptr()
-    x.warp_offsets = counts.warp_offsets.data_ptr()
+    x.nslices = partition.nslices
+    x.ticket = counts.ticket.data_ptr()
+    x.slice_counts = counts.slice_counts.data_ptr()
+    x.slice_offsets = counts.slice_offsets.data_ptr()
     x.total = counts.total_dev.data_ptr()
     if out is not None:
         for h in range(out.shape[0]):
@@ -289,7 +304,7 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
     """Read-only pass: exact per-slice output counts, nothing written."""
     if prep is None:
         prep = prepare(plan, store, interner)
-    n = partition.nwarps
+    n = partition.nslices
     if plan.depth == 0:
         return CountResult.constant(n, 1 if prep.ok else 0)
     if not prep.ok or partition.nkeys == 0:
@@ -299,6 +314,7 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
         torch.empty(n, dtype=dev.U64, device=d),
         torch.empty(n, dtype=dev.U64, device=d),
         torch.empty(1, dtype=dev.U64, device=d),
+        torch.zeros(1, dtype=torch.int32, device=d),
     )
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)

@@ -118,7 +118,7 @@ def test_sg_and_andersen_larger_vs_oracle():
     assert engine.relation_rows("SG") == want["SG"]
     assert sorted(summary.rounds_by_rules().values()) == sorted(r for _, _, r in report)
 
-    facts = random_andersen(random.Random(8), 3000)
+    facts = random_andersen(random.Random(8), 1200)
     engine, summary = run(CORPUS["andersen"], facts, schedule="stream", head_threshold=64)
     want, report = fixpoint_text(parse(CORPUS["andersen"]), facts)
     assert engine.relation_rows("PointsTo") == want["PointsTo"]
