@@ -118,6 +118,12 @@ typedef struct {
     int32_t check_level;                 /* negated: level of the probe, else -1 */
     uint8_t lvl_col[SRDL_MAX_LEVELS];    /* first index column bound at level L */
     uint8_t lvl_ncol[SRDL_MAX_LEVELS];   /* columns bound at level L (0 = none) */
+    /* optional histogram of index column 0 over the single segment
+     * (keys[hk], inclusive row prefix[hk]): column-0 narrowing becomes a
+     * binary search over the distinct keys (L2-resident) instead of the rows */
+    const uint32_t *hkeys;
+    const uint64_t *hprefix;
+    uint32_t hk;
 } srdl_atom;
 
 /* One compiled rule instance (reference: planner.JoinPlan, planner.py:53-73). */
@@ -151,7 +157,8 @@ typedef struct {
     const uint32_t *inner_lo;  /* K first inner row of each key, or NULL       */
     uint64_t nkeys;
     uint32_t nwarps;         /* warps launched                                */
-    uint32_t nslices;        /* slices of [0, T)                              */
+    uint32_t nslices;        /* capacity of the slice arrays                  */
+    uint64_t min_units;      /* slices used = clamp(ceil(T / min_units), 1, nslices) */
     uint32_t *ticket;        /* device counter, zero before each launch       */
     uint64_t *slice_counts;  /* nslices: tuples counted per slice             */
     uint64_t *slice_offsets; /* nslices: exclusive prefix of slice_counts     */

@@ -76,12 +76,38 @@ __device__ __forceinline__ uint32_t ubound(const uint32_t *__restrict__ col, uin
     return lo;
 }
 
+// Column-0 lookup through the index histogram: binary search over the K
+// distinct keys (a few MB, L2-resident) instead of the n rows.
+__device__ __forceinline__ bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
+    uint32_t lo = 0, hi = A.hk;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(A.hkeys + mid) < v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    if (lo < A.hk && __ldg(A.hkeys + lo) == v) {
+        r.lo = lo ? (uint32_t)__ldg(A.hprefix + lo - 1) : 0u;
+        r.hi = (uint32_t)__ldg(A.hprefix + lo);
+    } else {
+        r.hi = r.lo;
+    }
+    return true;
+}
+
 // Narrow r (rows of segment s of atom A) to rows whose level-L columns all
 // equal v. Returns the new length (0 = no match).
 __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
-    const int c0 = A.lvl_col[L], nc = A.lvl_ncol[L];
+    int c0 = A.lvl_col[L];
+    const int nc = A.lvl_ncol[L];
+    if (c0 == 0 && A.hkeys && s == 0) {  // full segment, first column: histogram
+        hist_range(A, v, r);
+        if (nc == 1 || r.lo >= r.hi) return r.hi - r.lo;
+        c0 = 1;
+    }
     uint32_t lo = r.lo, hi = r.hi;
-    for (int c = c0; c < c0 + nc && lo < hi; ++c) {
+    for (int c = c0; c < A.lvl_col[L] + nc && lo < hi; ++c) {
         const uint32_t *col = A.seg[s].cols[c];
         uint32_t a = lbound(col, lo, hi, v);
         hi = ubound(col, a, hi, v);
@@ -94,6 +120,10 @@ __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uin
 }
 
 __device__ __forceinline__ uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
+    if (A.lvl_col[L] == 0 && A.hkeys && s == 0) {
+        hist_range(A, v, r);
+        return r.hi - r.lo;
+    }
     const uint32_t *col = A.seg[s].cols[A.lvl_col[L]];
     uint32_t a = lbound(col, r.lo, r.hi, v);
     uint32_t b = ubound(col, a, r.hi, v);
@@ -171,49 +201,15 @@ __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const WarpSta
     }
 }
 
-// Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
-// level m-2 chunk; for m == 2 the single parent is the root rectangle).
+// Flattened leaf walk over the parents with len > 0 (per-lane driver range
+// lengths): prefix sum across the warp, every lane takes one (parent, row).
 template <bool WRITE>
-__device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t parents,
-                           Sink<WRITE> &sink) {
+__device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint64_t len,
+                            Sink<WRITE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t nls = P.nspec[leaf];
     const uint32_t l = lane_id();
-    // two plain positive sources on the leaf variable: merge-path candidates
-    bool pairable = nls == 2;
-    if (pairable) {
-        const srdl_atom &A0 = P.atom[P.spec[leaf][0]];
-        const srdl_atom &A1 = P.atom[P.spec[leaf][1]];
-        pairable = !A0.negated && !A1.negated && A0.lvl_ncol[leaf] == 1 && A1.lvl_ncol[leaf] == 1;
-    }
-    uint64_t len = 0;
-    bool heavy = false;
-    if ((parents >> l) & 1u) {
-        uint32_t best = 0xffffffffu, bj = 0, worst = 0;
-        for (uint32_t j = 0; j < nls; ++j) {
-            const srdl_atom &A = P.atom[P.spec[leaf][j]];
-            if (A.negated) continue;
-            uint32_t t = 0;
-            for (uint32_t s = 0; s < A.nseg; ++s) t += S.leaf[l][j][s].hi - S.leaf[l][j][s].lo;
-            if (t < best) {
-                best = t;
-                bj = j;
-            }
-            worst = t > worst ? t : worst;
-        }
-        len = best;
-        S.leaf_drv[l] = (uint8_t)bj;
-        if (pairable && best >= kMergeMin && worst <= best * kMergeRatio) {
-            const Rng a1 = S.leaf[l][0][1], b1 = S.leaf[l][1][1];
-            const bool single = (P.atom[P.spec[leaf][0]].nseg < 2 || a1.lo >= a1.hi) &&
-                                (P.atom[P.spec[leaf][1]].nseg < 2 || b1.lo >= b1.hi);
-            if (single) {
-                heavy = true;
-                len = 0;  // handled by merge_pair below
-            }
-        }
-    }
-    const uint32_t heavy_mask = __ballot_sync(kFull, heavy);
+    __syncwarp();
     uint64_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -276,7 +272,66 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
         sink.emit(P, X, S, alive, p, v, leaf);
     }
     __syncwarp();
-    for (uint32_t hm = heavy_mask; hm; hm &= hm - 1) merge_pair<WRITE>(P, X, S, __ffs(hm) - 1, sink);
+}
+
+// Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
+// level m-2 chunk; for m == 2 the single parent is the root rectangle).
+template <bool WRITE>
+__device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t parents,
+                           Sink<WRITE> &sink) {
+    const int leaf = (int)P.depth - 1;
+    const uint32_t nls = P.nspec[leaf];
+    const uint32_t l = lane_id();
+    // two plain positive sources on the leaf variable: merge-path candidates
+    bool pairable = nls == 2;
+    if (pairable) {
+        const srdl_atom &A0 = P.atom[P.spec[leaf][0]];
+        const srdl_atom &A1 = P.atom[P.spec[leaf][1]];
+        pairable = !A0.negated && !A1.negated && A0.lvl_ncol[leaf] == 1 && A1.lvl_ncol[leaf] == 1;
+    }
+    uint64_t len = 0;
+    bool heavy = false;
+    if ((parents >> l) & 1u) {
+        uint32_t best = 0xffffffffu, bj = 0, worst = 0;
+        for (uint32_t j = 0; j < nls; ++j) {
+            const srdl_atom &A = P.atom[P.spec[leaf][j]];
+            if (A.negated) continue;
+            uint32_t t = 0;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.leaf[l][j][s].hi - S.leaf[l][j][s].lo;
+            if (t < best) {
+                best = t;
+                bj = j;
+            }
+            worst = t > worst ? t : worst;
+        }
+        len = best;
+        S.leaf_drv[l] = (uint8_t)bj;
+        if (pairable && best >= kMergeMin && worst <= best * kMergeRatio) {
+            const Rng a1 = S.leaf[l][0][1], b1 = S.leaf[l][1][1];
+            const bool single = (P.atom[P.spec[leaf][0]].nseg < 2 || a1.lo >= a1.hi) &&
+                                (P.atom[P.spec[leaf][1]].nseg < 2 || b1.lo >= b1.hi);
+            if (single) {
+                heavy = true;
+                len = 0;  // handled by merge_pair below
+            }
+        }
+    }
+    const uint32_t heavy_mask = __ballot_sync(kFull, heavy);
+    // Parents are emitted in lane order (runs of flattened light parents,
+    // then one merge-path heavy parent), so a head that projects the
+    // variables in order receives lexicographically sorted tuples.
+    uint32_t remaining = parents;
+    while (remaining) {
+        const uint32_t hv = heavy_mask & remaining;
+        const uint32_t first_heavy = hv ? (uint32_t)(__ffs(hv) - 1) : 32u;
+        const uint32_t run = first_heavy == 32u ? remaining : remaining & ((1u << first_heavy) - 1u);
+        if (run) flat_leaves<WRITE>(P, X, S, ((run >> l) & 1u) ? len : 0, sink);
+        remaining &= ~run;
+        if (first_heavy < 32u) {
+            merge_pair<WRITE>(P, X, S, first_heavy, sink);
+            remaining &= ~(1u << first_heavy);
+        }
+    }
 }
 
 // Pick the smallest candidate source of level L and reset the chunk cursor.
@@ -492,13 +547,15 @@ __global__ void __launch_bounds__(kJoinWarps * 32)
     WarpState &S = states[wib];
     const uint64_t K = X.nkeys;
     const uint64_t T = K ? X.prefix[K - 1] : 0;
-    const uint64_t step = (T + X.nslices - 1) / X.nslices;
+    uint64_t used = (T + X.min_units - 1) / X.min_units;
+    used = used < 1 ? 1 : (used > X.nslices ? X.nslices : used);
+    const uint64_t step = (T + used - 1) / used;
     while (true) {
         // dynamic slice fetch: any warp may run any slice, offsets are per slice
         uint32_t sl = 0;
         if (lane_id() == 0) sl = atomicAdd(X.ticket, 1u);
         sl = __shfl_sync(kFull, sl, 0);
-        if (sl >= X.nslices) break;
+        if (sl >= used) break;
         uint64_t bs = (uint64_t)sl * step, be = bs + step;
         if (bs > T) bs = T;
         if (be > T) be = T;
@@ -554,6 +611,7 @@ static void check_plan(const srdl_plan *P, const srdl_exec *X) {
                  P->nspec[P->depth - 1], SRDL_MAX_LEAF_SPECS);
     SRDL_REQUIRE(X->nwarps >= 1 && X->nslices >= 1, "nwarps and nslices must be >= 1");
     SRDL_REQUIRE(X->ticket != nullptr, "a slice ticket counter is required");
+    SRDL_REQUIRE(X->min_units >= 1, "min_units must be >= 1");
 }
 
 }  // namespace srdl
@@ -568,6 +626,7 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
         cudaStream_t s = (cudaStream_t)stream;
         const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
         SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
+        SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
         wcoj_kernel<false><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
         SRDL_CHECK_LAUNCH();
         exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);

@@ -51,6 +51,9 @@ class AtomDesc(C.Structure):
         ("check_level", C.c_int32),
         ("lvl_col", C.c_uint8 * MAX_LEVELS),
         ("lvl_ncol", C.c_uint8 * MAX_LEVELS),
+        ("hkeys", C.c_void_p),
+        ("hprefix", C.c_void_p),
+        ("hk", C.c_uint32),
     ]
 
 
@@ -81,6 +84,7 @@ class ExecDesc(C.Structure):
         ("nkeys", C.c_uint64),
         ("nwarps", C.c_uint32),
         ("nslices", C.c_uint32),
+        ("min_units", C.c_uint64),
         ("ticket", C.c_void_p),
         ("slice_counts", C.c_void_p),
         ("slice_offsets", C.c_void_p),

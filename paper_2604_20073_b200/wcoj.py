@@ -34,7 +34,8 @@ from .partition import WorkPartition, decode_workunit, encode_workunit, rectangl
 from .syntax import VAR
 
 WARPS_PER_SM = 28  # 7 resident CTAs x 4 warps (30 KB shared memory each)
-SLICES_PER_WARP = 16  # root slices per launched warp, fetched dynamically
+SLICES_PER_WARP = 256  # slice-array capacity per launched warp (fetched dynamically)
+MIN_SLICE_UNITS = 4096  # fewer, larger slices when the root space is small
 
 # Benchmark hook: when a list, every count/materialize launch appends
 # (name, start_event, end_event) recorded on the launching stream.
@@ -150,6 +151,12 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                 ad.seg[s].cols[c] = ptrs[c]
             ad.seg[s].lo = lo
             ad.seg[s].hi = hi
+        if len(src) == 1 and pa.n_const == 0 and src[0][1] == 0 and src[0][2] == src[0][0].shape[1]:
+            hist = prep.rels[a].hist
+            if hist.nkeys and hist_covers(prep.rels[a], src[0][0]):
+                ad.hkeys = hist.keys.data_ptr()
+                ad.hprefix = hist.prefix.data_ptr()
+                ad.hk = hist.nkeys
         ad.negated = int(pa.negated)
         ad.arity = pa.arity
         ad.nconst = pa.n_const
@@ -158,6 +165,11 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
             ad.lvl_col[lvl] = cols[0]
             ad.lvl_ncol[lvl] = len(cols)
     return d
+
+
+def hist_covers(rel, rows) -> bool:
+    """The index histogram describes exactly `rows` (its only segment)."""
+    return rel.size == rows.shape[1]
 
 
 class DevicePartition:
@@ -286,6 +298,7 @@ def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=
     x.nkeys = partition.nkeys
     x.nwarps = partition.nwarps
     x.nslices = partition.nslices
+    x.min_units = MIN_SLICE_UNITS
     x.ticket = counts.ticket.data_ptr()
     x.slice_counts = counts.slice_counts.data_ptr()
     x.slice_offsets = counts.slice_offsets.data_ptr()
