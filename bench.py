@@ -129,39 +129,63 @@ class TriangleRMAT(Workload):
         return edge_bytes, 12 * n_out
 
 
-class TCRandom(Workload):
-    name = "tc-random"
-    program = TC
-    output = "TC"
+class Recursive(Workload):
+    """A recursive BASELINE workload: integer-column EDB from
+    paper_2604_20073_b200.suites, evaluated to fixpoint; the CPU sample is
+    the oracle on a scaled-down instance of the same generator."""
 
-    def __init__(self, nodes=10_000, edges=50_000, seed=1, rank=0, world=1):
-        self.nodes, self.nedges, self.seed, self.rank, self.world = nodes, edges, seed, rank, world
-        self.config = {"workload": f"transitive closure on a random digraph {nodes} nodes / {edges} edges"}
+    def __init__(self, name, rank=0, world=1, small=False):
+        from paper_2604_20073_b200 import suites
+
+        self.name = name
+        self.rank, self.world, self.small = rank, world, small
+        self.program, self.output = suites.BASELINE_PROGRAMS[name]
+        full, sample, desc = {
+            "tc": (lambda: suites.tc_random(10_000, 50_000, seed=1),
+                   lambda: suites.tc_random(1_000, 5_000, seed=1),
+                   "transitive closure on a random digraph, 10K nodes / 50K edges (configs[0])"),
+            "sg": (lambda: suites.sg_layered(levels=128, width=31_250, seed=0),
+                   lambda: suites.sg_layered(levels=24, width=2_000, seed=0),
+                   "same generation on a layered tree-plus-cross-edges graph, 128 levels x "
+                   "31250 nodes, ~4.3M edges (configs[2])"),
+            "andersen": (lambda: suites.andersen_modular(10_000_000, seed=1),
+                         lambda: suites.andersen_modular(8_000, seed=1),
+                         "Andersen points-to over modular synthetic programs, 10M statements "
+                         "(configs[3])"),
+        }[name]
+        self._full, self._sample = full, sample
+        self.config = {"workload": desc, "program_output": self.output}
 
     def generate(self):
         import torch
 
         from paper_2604_20073_b200 import device as dev
 
-        rng = np.random.default_rng(self.seed)
-        seen = set()
-        src, dst = [], []
-        while len(src) < self.nedges:
-            a, b = rng.integers(0, self.nodes, 2)
-            if a != b and (a, b) not in seen:
-                seen.add((a, b))
-                src.append(a)
-                dst.append(b)
-        e = torch.from_numpy(np.array([src, dst], dtype=np.uint32)).to(dev.device())
-        e = dev.sort_dedup(e, 32)
-        self.config["edges"] = int(e.shape[1])
-        return {"Edge": e}
+        facts = (self._sample if self.small else self._full)()
+        self.config["edb_facts"] = int(sum(v.shape[1] for v in facts.values()))
+        return {k: torch.from_numpy(v).to(dev.device()) for k, v in facts.items()}
 
     def algorithmic_bytes(self, inputs, n_out):
         return 8 * sum(int(t.shape[1]) for t in inputs.values()), 8 * n_out
 
+    def cpu_sample(self):
+        from oracle.gj import Symbols, fixpoint
+        from paper_2604_20073_b200 import parse
 
-WORKLOADS = {"triangle": TriangleRMAT, "tc": TCRandom}
+        facts = self._sample()
+        edb = {k: v.T.astype(np.int64) for k, v in facts.items()}
+        top = max(int(v.max()) for v in edb.values() if v.size) + 1
+        t0 = time.perf_counter()
+        rels, _ = fixpoint(parse(self.program), edb, Symbols(top))
+        dt = time.perf_counter() - t0
+        n = len(rels[self.output])
+        edb_n = sum(len(v) for v in edb.values())
+        return n, dt, (f"full fixpoint of a scaled-down instance of the same generator "
+                       f"({edb_n} EDB facts -> {n} {self.output} tuples in {dt:.2f} s), numpy "
+                       "semi-naive generic-join restatement of the reference")
+
+
+WORKLOADS = {"triangle": TriangleRMAT, "tc": "tc", "sg": "sg", "andersen": "andersen"}
 
 
 # --------------------------------------------------------------------------
@@ -404,10 +428,9 @@ def bench_ours(args, rank, world, dist):
 
 
 def make_workload(args, rank, world):
-    cls = WORKLOADS[args.workload]
     if args.workload == "triangle":
-        return cls(scale=args.scale or 20, edges=args.edges or 16_000_000, rank=rank, world=world)
-    return cls(rank=rank, world=world)
+        return TriangleRMAT(scale=args.scale or 20, edges=args.edges or 16_000_000, rank=rank, world=world)
+    return Recursive(args.workload, rank=rank, world=world, small=bool(args.small))
 
 
 # --------------------------------------------------------------------------
@@ -446,6 +469,17 @@ def cpu_sample(wl, inputs_host, target_s=12.0, seed=0):
         take = min(len(roots), int(take * max(2.0, target_s / max(dt, 1e-3) / 2)))
 
 
+def cpu_baseline(wl, inputs):
+    if isinstance(wl, TriangleRMAT):
+        host = {k: v.cpu().numpy().astype(np.int64).T for k, v in inputs.items()}
+        n, dt, take, nroots = cpu_sample(wl, host)
+        sample = (f"{take}/{nroots} random root keys, {n} derived tuples in {dt:.2f} s "
+                  "(numpy generic-join restatement of the reference executor)")
+    else:
+        n, dt, sample = wl.cpu_sample()
+    return {"value": n / dt, "unit": "tuples/s", "cores": 1, "kind": "port", "sample": sample}
+
+
 def bench_reference(args, rank, world):
     """--impl reference: the oracle port of the reference CPU algorithm."""
     import torch
@@ -454,15 +488,22 @@ def bench_reference(args, rank, world):
         return None
     wl = make_workload(args, 0, 1)
     torch.cuda.set_device(0) if torch.cuda.is_available() else None
-    inputs = {k: v.cpu().numpy().astype(np.int64).T for k, v in wl.generate().items()}
     rates = []
-    n = dt = take = nroots = 0
-    for i in range(args.warmup + args.steps):
-        n, dt, take, nroots = cpu_sample(wl, inputs, target_s=8.0, seed=i)
-        if i >= args.warmup:
-            rates.append(n / dt)
+    sample = ""
+    dt = 0.0
+    if isinstance(wl, TriangleRMAT):
+        inputs = {k: v.cpu().numpy().astype(np.int64).T for k, v in wl.generate().items()}
+        for i in range(args.warmup + args.steps):
+            n, dt, take, nroots = cpu_sample(wl, inputs, target_s=8.0, seed=i)
+            if i >= args.warmup:
+                rates.append(n / dt)
+        sample = f"{take}/{nroots} random root keys per step (generic join over the sample)"
+    else:
+        for i in range(1 + args.steps):  # one warm-up suffices for the CPU port
+            n, dt, sample = wl.cpu_sample()
+            if i >= 1:
+                rates.append(n / dt)
     value = sum(rates) / len(rates)
-    sample = f"{take}/{nroots} random root keys per step (generic join over the sample)"
     return {
         "impl": "reference",
         "metric": "derived tuples/sec (fixpoint)",
@@ -493,6 +534,7 @@ def main():
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (testing)")
     ap.add_argument("--edges", type=int, default=None, help="R-MAT edge count override (testing)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--small", action="store_true", help="recursive workloads: the CPU-sample instance")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -516,16 +558,7 @@ def main():
 
     result, wl, inputs = bench_ours(args, rank, world, dist)
     if rank == 0 and not args.no_cpu_baseline:
-        host = {k: v.cpu().numpy().astype(np.int64).T for k, v in inputs.items() if not k.startswith("_")}
-        n, dt, take, nroots = cpu_sample(wl, host)
-        result["cpu_baseline"] = {
-            "value": n / dt,
-            "unit": "tuples/s",
-            "cores": 1,
-            "kind": "port",
-            "sample": f"{take}/{nroots} random root keys, {n} derived tuples in {dt:.2f} s "
-                      "(numpy generic-join restatement of the reference executor)",
-        }
+        result["cpu_baseline"] = cpu_baseline(wl, inputs)
     if dist:
         dist.destroy_process_group()
     if rank == 0:

@@ -216,10 +216,14 @@ class DevicePartition:
             p or self.p,
         )
 
-    def slice_sizes(self) -> list:
-        t, n = self.total, self.nslices
-        step = -(-t // n) if t else 0
-        return [max(0, min((w + 1) * step, t) - min(w * step, t)) for w in range(n)]
+    def slices_used(self) -> int:
+        """Slices the kernels cut [0, T) into (csrc/wcoj.cu `used`)."""
+        used = -(-self.total // MIN_SLICE_UNITS)
+        return min(max(used, 1), self.nslices)
+
+    def max_slice(self) -> int:
+        t = self.total
+        return -(-t // self.slices_used()) if t else 0
 
 
 def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None, interner=None):

@@ -64,7 +64,7 @@ def test_golden_joins_through_execute_plan(golden, audited):
         assert host.shape[1] == case["emitted"], case["seed"]
     assert len(audited.traces) >= 150
     for t in audited.traces:
-        assert sum(t.tc) == t.total
+        assert t.tc_total == t.total
         assert t.bitmap_ok is not False
         assert t.aux_peak == t.total
         if t.work_total >= t.p:
