@@ -96,6 +96,12 @@ int srdl_histogram_merge(const uint32_t *ka, const uint32_t *da, uint64_t na, co
                          const uint32_t *db, uint64_t nb, uint32_t *keys, uint32_t *degrees,
                          uint64_t *prefix, uint64_t *k_out, void *stream);
 
+/* Dense column-0 offsets from a histogram (keys[K], inclusive prefix[K]):
+ * off[v] = number of rows whose column 0 is < v, for v in [0, n_ids];
+ * off has n_ids + 1 entries. The CSR row index of a sorted relation. */
+int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nkeys,
+                       uint32_t n_ids, uint32_t *off, void *stream);
+
 /* Narrow one sorted segment on its leading columns to constant values
  * (reference: executor.prepare constant narrowing, executor.py:188-206,
  * storage.narrow_segments, storage.py:122). Returns [*lo, *hi) on the host. */
@@ -124,6 +130,10 @@ typedef struct {
     const uint32_t *hkeys;
     const uint64_t *hprefix;
     uint32_t hk;
+    /* optional dense column-0 offsets over the single segment: rows with
+     * column 0 == v are [doff[v], doff[v+1]) for v < dn (two loads) */
+    uint32_t dn;
+    const uint32_t *doff;
 } srdl_atom;
 
 /* One compiled rule instance (reference: planner.JoinPlan, planner.py:53-73). */

@@ -160,6 +160,20 @@ __global__ void narrow_prefix_kernel(Cols cols, uint64_t n, const uint32_t *__re
     range[1] = hi;
 }
 
+__global__ void dense_offsets_kernel(const uint32_t *__restrict__ keys,
+                                     const uint64_t *__restrict__ prefix, uint64_t nk,
+                                     uint32_t n_ids, uint32_t *__restrict__ off) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n_ids;
+         v += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = nk;  // first key >= v
+        while (lo < hi) {
+            uint64_t m = (lo + hi) >> 1;
+            if (keys[m] < v) lo = m + 1; else hi = m;
+        }
+        off[v] = lo ? (uint32_t)prefix[lo - 1] : 0u;
+    }
+}
+
 // counter-based RNG: splitmix64 finaliser over (seed, edge, level)
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 30;
@@ -302,6 +316,16 @@ int srdl_root_work(const uint32_t *okeys, const uint32_t *odeg, const uint64_t *
                                                               outer_lo, inner_lo);
         SRDL_CHECK_LAUNCH();
         inclusive_scan_u64(prefix, prefix, nk, s);
+    });
+}
+
+int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nkeys,
+                       uint32_t n_ids, uint32_t *off, void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        dense_offsets_kernel<<<stride_grid((uint64_t)n_ids + 1), kThreads, 0, s>>>(keys, prefix, nkeys,
+                                                                                  n_ids, off);
+        SRDL_CHECK_LAUNCH();
     });
 }
 

@@ -98,11 +98,24 @@ __device__ __forceinline__ bool hist_range(const srdl_atom &A, uint32_t v, Rng &
 
 // Narrow r (rows of segment s of atom A) to rows whose level-L columns all
 // equal v. Returns the new length (0 = no match).
+__device__ __forceinline__ void col0_range(const srdl_atom &A, uint32_t v, Rng &r) {
+    if (A.doff) {  // dense CSR offsets: two loads
+        if (v < A.dn) {
+            r.lo = __ldg(A.doff + v);
+            r.hi = __ldg(A.doff + v + 1);
+        } else {
+            r.hi = r.lo;
+        }
+    } else {
+        hist_range(A, v, r);
+    }
+}
+
 __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
     int c0 = A.lvl_col[L];
     const int nc = A.lvl_ncol[L];
-    if (c0 == 0 && A.hkeys && s == 0) {  // full segment, first column: histogram
-        hist_range(A, v, r);
+    if (c0 == 0 && (A.hkeys || A.doff) && s == 0) {  // full segment, first column
+        col0_range(A, v, r);
         if (nc == 1 || r.lo >= r.hi) return r.hi - r.lo;
         c0 = 1;
     }
@@ -120,8 +133,8 @@ __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uin
 }
 
 __device__ __forceinline__ uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
-    if (A.lvl_col[L] == 0 && A.hkeys && s == 0) {
-        hist_range(A, v, r);
+    if (A.lvl_col[L] == 0 && (A.hkeys || A.doff) && s == 0) {
+        col0_range(A, v, r);
         return r.hi - r.lo;
     }
     const uint32_t *col = A.seg[s].cols[A.lvl_col[L]];
@@ -547,7 +560,11 @@ __global__ void __launch_bounds__(kJoinWarps * 32)
     WarpState &S = states[wib];
     const uint64_t K = X.nkeys;
     const uint64_t T = K ? X.prefix[K - 1] : 0;
+    // enough slices to occupy every launched warp several times, coarser
+    // ones (>= min_units units) only when T is large
     uint64_t used = (T + X.min_units - 1) / X.min_units;
+    const uint64_t floor_slices = (uint64_t)X.nwarps * 4 < T ? (uint64_t)X.nwarps * 4 : T;
+    if (used < floor_slices) used = floor_slices;
     used = used < 1 ? 1 : (used > X.nslices ? X.nslices : used);
     const uint64_t step = (T + used - 1) / used;
     while (true) {

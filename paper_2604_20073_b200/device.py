@@ -54,6 +54,8 @@ class AtomDesc(C.Structure):
         ("hkeys", C.c_void_p),
         ("hprefix", C.c_void_p),
         ("hk", C.c_uint32),
+        ("dn", C.c_uint32),
+        ("doff", C.c_void_p),
     ]
 
 
@@ -128,6 +130,9 @@ _SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
          C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_dense_offsets": (
+        C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]
     ),
     "srdl_narrow_prefix": (
         C.c_int,
@@ -339,6 +344,15 @@ def histogram_merge(ka, da, kb, db):
                                      C.byref(k), stream_handle()), "histogram_merge")
     K = k.value
     return keys[:K], deg[:K], prefix[:K]
+
+
+def dense_offsets(keys, prefix, n_ids: int) -> torch.Tensor:
+    """CSR offsets of a sorted column from its histogram (n_ids + 1 entries)."""
+    off = torch.empty(n_ids + 1, dtype=U32, device=device())
+    check(lib().srdl_dense_offsets(keys.data_ptr() if keys.numel() else None,
+                                   prefix.data_ptr() if prefix.numel() else None, keys.numel(),
+                                   n_ids, off.data_ptr(), stream_handle()), "dense_offsets")
+    return off
 
 
 def narrow_prefix(rows: torch.Tensor, lo: int, hi: int, values) -> tuple:

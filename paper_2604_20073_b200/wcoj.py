@@ -66,14 +66,15 @@ def _resolve(store, pa):
 class Prepared:
     """Read-only device view of one plan execution's sources."""
 
-    __slots__ = ("plan", "rels", "segs", "ok", "head_resolved", "_desc")
+    __slots__ = ("plan", "rels", "segs", "ok", "head_resolved", "n_ids", "_desc")
 
-    def __init__(self, plan, rels, segs, ok, head_resolved):
+    def __init__(self, plan, rels, segs, ok, head_resolved, n_ids=0):
         self.plan = plan
         self.rels = rels
         self.segs = segs  # per atom: [(rows tensor, lo, hi), ...] body first
         self.ok = ok
         self.head_resolved = head_resolved
+        self.n_ids = n_ids  # ids are < n_ids (symbol table size)
         self._desc = None
 
     def descriptor(self) -> dev.PlanDesc:
@@ -106,7 +107,7 @@ def prepare(plan: JoinPlan, store, interner) -> Prepared:
         if pa.negated and pa.check_level == -1 and src:
             ok = False
     head = tuple((True, x) if kind == VAR else (False, interner.intern(x)) for kind, x in plan.head_cols)
-    return Prepared(plan, rels, segs, ok, head)
+    return Prepared(plan, rels, segs, ok, head, len(interner))
 
 
 def encode_plan(prep: Prepared) -> dev.PlanDesc:
@@ -157,6 +158,10 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                 ad.hkeys = hist.keys.data_ptr()
                 ad.hprefix = hist.prefix.data_ptr()
                 ad.hk = hist.nkeys
+                dense = prep.rels[a].dense_offsets(prep.n_ids) if prep.n_ids else None
+                if dense is not None:
+                    ad.doff = dense.data_ptr()
+                    ad.dn = prep.n_ids
         ad.negated = int(pa.negated)
         ad.arity = pa.arity
         ad.nconst = pa.n_const
@@ -218,7 +223,7 @@ class DevicePartition:
 
     def slices_used(self) -> int:
         """Slices the kernels cut [0, T) into (csrc/wcoj.cu `used`)."""
-        used = -(-self.total // MIN_SLICE_UNITS)
+        used = max(-(-self.total // MIN_SLICE_UNITS), min(self.nwarps * 4, self.total))
         return min(max(used, 1), self.nslices)
 
     def max_slice(self) -> int:

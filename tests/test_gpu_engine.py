@@ -164,3 +164,28 @@ def test_max_iterations_watchdog():
     assert summary.relations["TC"] == 78
     with pytest.raises(InternalError):
         run(CORPUS["tc"], {"Edge": edges}, max_iterations=3)
+
+
+@pytest.mark.parametrize("suite", ["tc", "sg", "triangle", "star", "neg2hop", "andersen"])
+def test_reference_suites_verified(suite):
+    from paper_2604_20073_b200.suites import run_suite
+
+    def check(program, facts):
+        return fixpoint_text(program, facts)[0]
+
+    for schedule in ("seq", "stream"):
+        report = run_suite(suite, "small", 3, schedule=schedule, verify=check)
+        assert report["verified"] is True
+        assert report["phase_micros"].get("count", 0) > 0
+
+
+def test_dense_offsets_match_histogram():
+    from paper_2604_20073_b200 import device as dev
+    from paper_2604_20073_b200.columns import Histogram
+
+    rng = np.random.default_rng(2)
+    col = np.sort(rng.integers(0, 5000, 200_000)).astype(np.uint32)
+    h = Histogram.over_column(col)
+    off = dev.dense_offsets(h.keys, h.prefix, 6000).cpu().numpy().astype(np.int64)
+    want = np.searchsorted(col, np.arange(6001), side="left")
+    assert np.array_equal(off, want)
