@@ -61,8 +61,9 @@ int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uin
                     uint32_t *const *out, uint64_t *n_out, void *stream);
 
 /* reference: storage.compute_delta (storage.py:311): distinct staged rows
- * minus the rows of up to two sorted, duplicate-free segments of the full
- * relation (head and body). Fuses sort, unique and the anti-join.
+ * minus the rows of up to eight sorted, duplicate-free segments (the full
+ * relation's head and body, plus deltas of earlier chunks when a staging
+ * buffer exceeds 2^31 rows). Fuses sort, unique and the anti-join.
  * seg_cols[s] points to `arity` column pointers of segment s. */
 int srdl_compute_delta(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
                        const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,

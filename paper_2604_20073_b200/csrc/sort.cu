@@ -158,9 +158,11 @@ __device__ __forceinline__ uint64_t pack_row(const Cols &c, uint64_t j, uint32_t
     return k;
 }
 
+constexpr int kMaxDiffSegs = 8;  // head, body + earlier chunks of a large staging buffer
+
 struct Segs {
-    Cols seg[SRDL_MAX_SEGS];
-    uint64_t rows[SRDL_MAX_SEGS];
+    Cols seg[kMaxDiffSegs];
+    uint64_t rows[kMaxDiffSegs];
     uint32_t nseg;
 };
 
@@ -365,7 +367,7 @@ int srdl_compute_delta(const uint32_t *const *cols, uint32_t arity, uint64_t n, 
                        const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,
                        uint32_t nseg, uint32_t *const *out, uint64_t *n_out, void *stream) {
     return guarded([&] {
-        SRDL_REQUIRE(nseg <= SRDL_MAX_SEGS, "at most %d full segments", SRDL_MAX_SEGS);
+        SRDL_REQUIRE(nseg <= kMaxDiffSegs, "at most %d full segments", kMaxDiffSegs);
         Segs S{};
         S.nseg = 0;
         for (uint32_t q = 0; q < nseg; ++q) {

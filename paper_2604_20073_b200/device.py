@@ -30,6 +30,7 @@ MAX_COLS = 8
 MAX_HEAD = 12
 MAX_SEGS = 2
 MAX_LEAF_SPECS = 6
+MAX_DIFF_SEGS = 8
 NO_ATOM = 255
 NO_SYMBOL = 0xFFFFFFFF
 
@@ -269,9 +270,11 @@ def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
     if n == 0:
         return out
     segs = [s for s in segments if nrows(s)]
+    if len(segs) > MAX_DIFF_SEGS:
+        raise InternalError(f"compute_delta: at most {MAX_DIFF_SEGS} segments")
     seg_ptr_arrays = [col_ptrs(s) for s in segs]
-    seg_cols = (C.c_void_p * MAX_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
-    seg_rows = (C.c_uint64 * MAX_SEGS)(*[nrows(s) for s in segs])
+    seg_cols = (C.c_void_p * MAX_DIFF_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
+    seg_rows = (C.c_uint64 * MAX_DIFF_SEGS)(*[nrows(s) for s in segs])
     got = C.c_uint64(0)
     check(
         lib().srdl_compute_delta(col_ptrs(rows), arity, n, bits, seg_cols, seg_rows, len(segs),

@@ -122,3 +122,18 @@ def test_empty_and_single_rows(dev):
     assert dev.is_sorted_strict(one)
     top = to_dev([(0xFFFFFFFE, 0), (0, 0xFFFFFFFE), (0xFFFFFFFE, 0)], 2)
     assert host(dev.sort_dedup(top, 32)).tolist() == [[0, 0xFFFFFFFE], [0xFFFFFFFE, 0]]
+
+
+def test_compute_delta_chunked_equals_single(dev, monkeypatch):
+    from paper_2604_20073_b200 import columns
+
+    rng = np.random.default_rng(17)
+    full_rows = ost.sort_dedup(rng.integers(0, 500, size=(200_000, 2)))
+    rel = columns.ColumnarRelation.from_sorted(2, (0, 1), to_dev(full_rows, 2))
+    staged = to_dev(rng.integers(0, 700, size=(900_000, 2)), 2)
+    whole = columns.compute_delta(staged, rel)
+    monkeypatch.setattr(columns, "DELTA_CHUNK", 70_001)  # 13 chunks, exercises the re-merge
+    chunked = columns.compute_delta(staged, rel)
+    assert torch.equal(whole, chunked)
+    want = ost.compute_delta(host(staged), np.empty((0, 2), np.int64), full_rows)
+    assert np.array_equal(host(chunked), want)

@@ -1,0 +1,53 @@
+"""Diagnostics: per-phase device times of one fixpoint (Stats enabled).
+
+    python tools/phase_report.py --workload triangle|sg|tc|andersen [--statements N]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+from paper_2604_20073_b200 import Engine, Stats, parse, suites
+from paper_2604_20073_b200 import device as dev
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="triangle")
+    ap.add_argument("--statements", type=int, default=1_000_000)
+    ap.add_argument("--schedule", default="stream")
+    args = ap.parse_args()
+    if args.workload == "triangle":
+        raw = dev.gen_rmat(20, 16_000_000, seed=1).view(torch.int32)
+        raw = raw[:, raw[0] != raw[1]].contiguous().view(torch.uint32)
+        e = dev.sort_dedup(raw, 20)
+        facts = {"R": e, "S": e, "T": e}
+        program, out = suites.TRIANGLE_PROGRAM, "Triangle"
+    else:
+        gen = {"sg": lambda: suites.sg_layered(),
+               "tc": lambda: suites.tc_random(),
+               "andersen": lambda: suites.andersen_modular(args.statements, seed=1)}[args.workload]
+        facts = {k: torch.from_numpy(v).cuda() for k, v in gen().items()}
+        program, out = suites.BASELINE_PROGRAMS[args.workload]
+    for rep in range(2):
+        stats = Stats()
+        eng = Engine(parse(program), schedule=args.schedule, stats=stats)
+        for k, v in facts.items():
+            eng.load_columns(k, v)
+        t0 = time.perf_counter()
+        summ = eng.solve()
+        wall = time.perf_counter() - t0
+        totals = {k: round(v / 1e3, 2) for k, v in sorted(stats.phase_totals().items(), key=lambda x: -x[1])}
+        print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "out": summ.relations[out],
+                          "iterations": [s.iterations for s in summ.strata],
+                          "phase_ms": totals}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
