@@ -406,6 +406,7 @@ def bench_ours(args, rank, world, dist):
         "warmup": args.warmup,
         "ms_per_step": step_s * 1e3,
         "fixpoint_wall_s": step_s,
+        "step_ms_each": [round(t * 1e3, 2) for t in times],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,

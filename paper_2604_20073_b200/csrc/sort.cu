@@ -9,6 +9,7 @@
 // split into chunks of at most 64 bits, sorted least-significant chunk first
 // with a stable radix sort carrying a row permutation.
 #include "common.cuh"
+#include "mergepath.cuh"
 
 namespace srdl {
 
@@ -166,41 +167,12 @@ struct Segs {
     uint32_t nseg;
 };
 
-__device__ __forceinline__ bool segs_contain_key(const Segs &S, uint64_t key, uint32_t arity,
-                                                 uint32_t bits) {
-    for (uint32_t s = 0; s < S.nseg; ++s) {
-        uint64_t lo = 0, hi = S.rows[s];
-        while (lo < hi) {
-            uint64_t mid = lo + ((hi - lo) >> 1);
-            if (pack_row(S.seg[s], mid, arity, bits) < key)
-                lo = mid + 1;
-            else
-                hi = mid;
-        }
-        if (lo < S.rows[s] && pack_row(S.seg[s], lo, arity, bits) == key) return true;
-    }
-    return false;
-}
-
-__device__ __forceinline__ bool segs_contain_row(const Segs &S, const Cols &A, uint64_t i,
-                                                 uint32_t arity) {
-    for (uint32_t s = 0; s < S.nseg; ++s) {
-        uint64_t pos = row_bound(S.seg[s], 0, S.rows[s], A, i, arity, false);
-        if (pos < S.rows[s] && row_cmp(S.seg[s], pos, A, i, arity) == 0) return true;
-    }
-    return false;
-}
-
-// keep[i] = first of its run of equal keys and absent from the full segments
-__global__ void flag_keys(const uint64_t *__restrict__ keys, uint64_t n, Segs S, uint32_t arity,
-                          uint32_t bits, uint32_t *__restrict__ keep) {
+// keep[i] = first of its run of equal keys (membership in the full
+// segments is removed afterwards by the merge-path anti-join)
+__global__ void flag_keys(const uint64_t *__restrict__ keys, uint64_t n, uint32_t *__restrict__ keep) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t k = keys[i];
-        bool f = (i == 0) || keys[i - 1] != k;
-        if (f && S.nseg) f = !segs_contain_key(S, k, arity, bits);
-        keep[i] = f;
-    }
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keep[i] = (i == 0) || keys[i - 1] != keys[i];
 }
 
 __global__ void scatter_unpack(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ keep,
@@ -219,13 +191,28 @@ __global__ void scatter_unpack(const uint64_t *__restrict__ keys, const uint32_t
     }
 }
 
-// general path (arity*bits > 64): rows already gathered into sorted order
-__global__ void flag_rows(Cols rows, uint64_t n, Segs S, uint32_t arity, uint32_t *__restrict__ keep) {
+// general path (arity*bits > 64 or presorted input): run starts of sorted rows
+__global__ void flag_rows(Cols rows, uint64_t n, uint32_t arity, uint32_t *__restrict__ keep) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        bool f = (i == 0) || row_cmp(rows, i - 1, rows, i, arity) != 0;
-        if (f && S.nseg) f = !segs_contain_row(S, rows, i, arity);
-        keep[i] = f;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keep[i] = (i == 0) || row_cmp(rows, i - 1, rows, i, arity) != 0;
+}
+
+static void anti_join_keys(const uint64_t *keys, uint64_t n, const Segs &S, uint32_t arity,
+                           uint32_t bits, uint32_t *keep, cudaStream_t s) {
+    for (uint32_t q = 0; q < S.nseg; ++q) {
+        PackedRows B{S.seg[q], arity, bits};
+        mp_diff_keys<<<mp_grid(n + S.rows[q]), kThreads, 0, s>>>(keys, n, B, S.rows[q], keep);
+        SRDL_CHECK_LAUNCH();
+    }
+}
+
+static void anti_join_rows(const Cols &rows, uint64_t n, const Segs &S, uint32_t arity,
+                           uint32_t *keep, cudaStream_t s) {
+    for (uint32_t q = 0; q < S.nseg; ++q) {
+        mp_diff_rows<<<mp_grid(n + S.rows[q]), kThreads, 0, s>>>(rows, n, S.seg[q], S.rows[q], arity,
+                                                                keep);
+        SRDL_CHECK_LAUNCH();
     }
 }
 
@@ -292,8 +279,9 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
     if (rows_sorted(in, n, arity, false, s)) {
         // staged rows already in index order (e.g. WCOJ output enumerated in
         // variable order): unique + anti-join without sorting
-        flag_rows<<<g, kThreads, 0, s>>>(in, n, S, arity, keep.as<uint32_t>());
+        flag_rows<<<g, kThreads, 0, s>>>(in, n, arity, keep.as<uint32_t>());
         SRDL_CHECK_LAUNCH();
+        anti_join_rows(in, n, S, arity, keep.as<uint32_t>(), s);
         Scratch pos(n * sizeof(uint32_t), s);
         exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
         scatter_rows<<<g, kThreads, 0, s>>>(in, keep.as<uint32_t>(), pos.as<uint32_t>(), n, arity, dst);
@@ -302,8 +290,9 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
         pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, arity}, bits, nullptr, n, keys.as<uint64_t>());
         SRDL_CHECK_LAUNCH();
         radix_sort(keys.as<uint64_t>(), nullptr, n, arity * bits, s);
-        flag_keys<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), n, S, arity, bits, keep.as<uint32_t>());
+        flag_keys<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), n, keep.as<uint32_t>());
         SRDL_CHECK_LAUNCH();
+        anti_join_keys(keys.as<uint64_t>(), n, S, arity, bits, keep.as<uint32_t>(), s);
         Scratch pos(n * sizeof(uint32_t), s);
         exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
         scatter_unpack<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), keep.as<uint32_t>(),
@@ -334,8 +323,9 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
         }
         gather_cols<<<g, kThreads, 0, s>>>(in, arity, perm.as<uint32_t>(), n, tmp);
         SRDL_CHECK_LAUNCH();
-        flag_rows<<<g, kThreads, 0, s>>>(tmpc, n, S, arity, keep.as<uint32_t>());
+        flag_rows<<<g, kThreads, 0, s>>>(tmpc, n, arity, keep.as<uint32_t>());
         SRDL_CHECK_LAUNCH();
+        anti_join_rows(tmpc, n, S, arity, keep.as<uint32_t>(), s);
         Scratch pos(n * sizeof(uint32_t), s);
         exclusive_scan_u32(keep.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
         scatter_rows<<<g, kThreads, 0, s>>>(tmpc, keep.as<uint32_t>(), pos.as<uint32_t>(), n, arity,
