@@ -1,9 +1,11 @@
-// Merge path over sorted row sets (Green, McColl & Bader, "GPU merge path").
-// Thread t owns output diagonals [t*kMergeItems, (t+1)*kMergeItems) of the
-// stable merge of A and B (A first on ties): one binary search finds where
-// its window starts, then it merges sequentially. Linear total work and
-// near-coalesced reads, used for
-//   * the head/body flush and head merges (merge of disjoint sets), and
+// Merge path over sorted row sets (Green, McColl & Bader, "GPU merge path"),
+// block-tiled. Block b owns output diagonals [b*kMT, (b+1)*kMT) of the
+// stable merge of A and B (A first on ties): thread 0 finds where the tile
+// starts and ends in A with two binary searches, the block loads both input
+// tiles into shared memory with coalesced reads, and each thread merges
+// kMI consecutive outputs from shared memory. Linear work, one global read
+// of every input element, coalesced writes. Used for
+//   * the head/body flush and head merges (merge of disjoint row sets), and
 //   * the anti-join of compute_delta (membership of every staged row in a
 //     full segment), replacing per-row binary searches.
 #pragma once
@@ -12,7 +14,8 @@
 
 namespace srdl {
 
-constexpr int kMergeItems = 32;
+constexpr int kMI = 4;                 // outputs per thread
+constexpr int kMT = kThreads * kMI;    // outputs per block tile (1024)
 
 // Rows of a segment read as packed keys (same layout as the staged keys).
 struct PackedRows {
@@ -39,69 +42,140 @@ __device__ __forceinline__ uint64_t mp_split(uint64_t d, uint64_t na, uint64_t n
     return lo;
 }
 
-// Merge two sorted row sets (ties: A first) into out.
-static __global__ void mp_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, MutCols out) {
-    const uint64_t n = na + nb;
+// Tile bounds: a0/a1 in A for this block's diagonal range (thread 0, smem).
+template <class LE>
+__device__ __forceinline__ void tile_bounds(uint64_t na, uint64_t nb, const LE &le, uint64_t *sh) {
+    if (threadIdx.x == 0) {
+        const uint64_t n = na + nb, d0 = (uint64_t)blockIdx.x * kMT;
+        const uint64_t d1 = d0 + kMT < n ? d0 + kMT : n;
+        sh[0] = mp_split(d0, na, nb, le);
+        sh[1] = mp_split(d1, na, nb, le);
+        sh[2] = d0;
+        sh[3] = d1;
+    }
+    __syncthreads();
+}
+
+// smem layout for row tiles: column c of tile row k at s[c * kMT + k];
+// A rows at [0, ta), B rows at [ta, ta + tb)
+__device__ __forceinline__ int smem_row_cmp(const uint32_t *s, uint32_t x, uint32_t y, uint32_t arity) {
+    for (uint32_t c = 0; c < arity; ++c) {
+        const uint32_t u = s[c * kMT + x], v = s[c * kMT + y];
+        if (u != v) return u < v ? -1 : 1;
+    }
+    return 0;
+}
+
+// Merge two sorted row sets (ties: A first) into out. Dynamic smem: arity*kMT*4.
+static __global__ void __launch_bounds__(kThreads)
+    mp_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, MutCols out) {
+    extern __shared__ uint32_t tile[];
+    __shared__ uint64_t sh[4];
     auto le = [&](uint64_t i, uint64_t j) { return row_cmp(A, i, B, j, arity) <= 0; };
-    for (uint64_t d0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kMergeItems; d0 < n;
-         d0 += (uint64_t)gridDim.x * blockDim.x * kMergeItems) {
-        uint64_t i = mp_split(d0, na, nb, le), j = d0 - i;
-        const uint64_t end = d0 + kMergeItems < n ? d0 + kMergeItems : n;
-        for (uint64_t d = d0; d < end; ++d) {
-            const bool take_a = j >= nb || (i < na && le(i, j));
-            const Cols &src = take_a ? A : B;
-            const uint64_t row = take_a ? i++ : j++;
-            for (uint32_t c = 0; c < arity; ++c) out.c[c][d] = __ldg(src.c[c] + row);
-        }
+    tile_bounds(na, nb, le, sh);
+    const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
+    const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
+    const uint64_t b0 = d0 - a0;
+    for (uint32_t c = 0; c < arity; ++c) {
+        for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads)
+            tile[c * kMT + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
+    }
+    __syncthreads();
+    const uint32_t k0 = threadIdx.x * kMI;
+    if (k0 >= ta + tb) return;
+    // split of this thread's diagonal inside the tile
+    uint32_t lo = k0 > tb ? k0 - tb : 0, hi = k0 < ta ? k0 : ta;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (smem_row_cmp(tile, mid, ta + (k0 - 1 - mid), arity) <= 0)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    uint32_t i = lo, j = k0 - lo;
+    const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
+    for (uint32_t k = k0; k < kend; ++k) {
+        const bool take_a = j >= tb || (i < ta && smem_row_cmp(tile, i, ta + j, arity) <= 0);
+        const uint32_t src = take_a ? i++ : ta + j++;
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][d0 + k] = tile[c * kMT + src];
     }
 }
 
 // keep[i] = 0 for every staged key present in the packed segment B.
-static __global__ void mp_diff_keys(const uint64_t *__restrict__ keys, uint64_t na, PackedRows B, uint64_t nb,
-                             uint32_t *__restrict__ keep) {
-    const uint64_t n = na + nb;
+static __global__ void __launch_bounds__(kThreads)
+    mp_diff_keys(const uint64_t *__restrict__ keys, uint64_t na, PackedRows B, uint64_t nb,
+                 uint32_t *__restrict__ keep) {
+    __shared__ uint64_t tile[kMT];
+    __shared__ uint64_t sh[4];
     auto le = [&](uint64_t i, uint64_t j) { return keys[i] <= B[j]; };
-    for (uint64_t d0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kMergeItems; d0 < n;
-         d0 += (uint64_t)gridDim.x * blockDim.x * kMergeItems) {
-        uint64_t i = mp_split(d0, na, nb, le), j = d0 - i;
-        const uint64_t end = d0 + kMergeItems < n ? d0 + kMergeItems : n;
-        uint64_t bj = j < nb ? B[j] : ~0ull;
-        for (uint64_t d = d0; d < end; ++d) {
-            if (i < na && (j >= nb || keys[i] <= bj)) {
-                if (j < nb && keys[i] == bj) keep[i] = 0;
-                ++i;
-            } else {
-                ++j;
-                bj = j < nb ? B[j] : ~0ull;
-            }
+    tile_bounds(na, nb, le, sh);
+    const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
+    const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
+    const uint64_t b0 = d0 - a0;
+    for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads) tile[k] = k < ta ? keys[a0 + k] : B[b0 + k - ta];
+    __syncthreads();
+    const uint32_t k0 = threadIdx.x * kMI;
+    if (k0 >= ta + tb) return;
+    uint32_t lo = k0 > tb ? k0 - tb : 0, hi = k0 < ta ? k0 : ta;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (tile[mid] <= tile[ta + (k0 - 1 - mid)])
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    uint32_t i = lo, j = k0 - lo;
+    const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
+    for (uint32_t k = k0; k < kend; ++k) {
+        if (i < ta && (j >= tb || tile[i] <= tile[ta + j])) {
+            if (j < tb && tile[i] == tile[ta + j]) keep[a0 + i] = 0;
+            ++i;
+        } else {
+            ++j;
         }
     }
 }
 
 // keep[i] = 0 for every staged row of A present in segment B (row compare).
-static __global__ void mp_diff_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity,
-                             uint32_t *__restrict__ keep) {
-    const uint64_t n = na + nb;
+// Dynamic smem: arity*kMT*4.
+static __global__ void __launch_bounds__(kThreads)
+    mp_diff_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, uint32_t *__restrict__ keep) {
+    extern __shared__ uint32_t tile[];
+    __shared__ uint64_t sh[4];
     auto le = [&](uint64_t i, uint64_t j) { return row_cmp(A, i, B, j, arity) <= 0; };
-    for (uint64_t d0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kMergeItems; d0 < n;
-         d0 += (uint64_t)gridDim.x * blockDim.x * kMergeItems) {
-        uint64_t i = mp_split(d0, na, nb, le), j = d0 - i;
-        const uint64_t end = d0 + kMergeItems < n ? d0 + kMergeItems : n;
-        for (uint64_t d = d0; d < end; ++d) {
-            int c = (i < na && j < nb) ? row_cmp(A, i, B, j, arity) : (i < na ? -1 : 1);
-            if (c <= 0) {
-                if (c == 0) keep[i] = 0;
-                ++i;
-            } else {
-                ++j;
-            }
+    tile_bounds(na, nb, le, sh);
+    const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
+    const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
+    const uint64_t b0 = d0 - a0;
+    for (uint32_t c = 0; c < arity; ++c) {
+        for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads)
+            tile[c * kMT + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
+    }
+    __syncthreads();
+    const uint32_t k0 = threadIdx.x * kMI;
+    if (k0 >= ta + tb) return;
+    uint32_t lo = k0 > tb ? k0 - tb : 0, hi = k0 < ta ? k0 : ta;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (smem_row_cmp(tile, mid, ta + (k0 - 1 - mid), arity) <= 0)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    uint32_t i = lo, j = k0 - lo;
+    const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
+    for (uint32_t k = k0; k < kend; ++k) {
+        const int c = (i < ta && j < tb) ? smem_row_cmp(tile, i, ta + j, arity) : (i < ta ? -1 : 1);
+        if (c <= 0) {
+            if (c == 0) keep[a0 + i] = 0;
+            ++i;
+        } else {
+            ++j;
         }
     }
 }
 
-inline unsigned mp_grid(uint64_t n) {
-    uint64_t threads = (n + kMergeItems - 1) / kMergeItems;
-    return stride_grid(threads);
-}
+inline unsigned mp_grid(uint64_t n) { return grid_for(n, kMT); }
+inline size_t mp_smem(uint32_t arity) { return (size_t)arity * kMT * sizeof(uint32_t); }
 
 }  // namespace srdl

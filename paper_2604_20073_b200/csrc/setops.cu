@@ -243,7 +243,7 @@ int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, 
         cudaStream_t s = (cudaStream_t)stream;
         Cols A = na ? make_cols(a, arity) : Cols{};
         Cols B = nb ? make_cols(b, arity) : Cols{};
-        mp_merge_rows<<<mp_grid(n), kThreads, 0, s>>>(A, na, B, nb, arity, make_mut(out, arity));
+        mp_merge_rows<<<mp_grid(n), kThreads, mp_smem(arity), s>>>(A, na, B, nb, arity, make_mut(out, arity));
         SRDL_CHECK_LAUNCH();
     });
 }

@@ -210,7 +210,7 @@ static void anti_join_keys(const uint64_t *keys, uint64_t n, const Segs &S, uint
 static void anti_join_rows(const Cols &rows, uint64_t n, const Segs &S, uint32_t arity,
                            uint32_t *keep, cudaStream_t s) {
     for (uint32_t q = 0; q < S.nseg; ++q) {
-        mp_diff_rows<<<mp_grid(n + S.rows[q]), kThreads, 0, s>>>(rows, n, S.seg[q], S.rows[q], arity,
+        mp_diff_rows<<<mp_grid(n + S.rows[q]), kThreads, mp_smem(arity), s>>>(rows, n, S.seg[q], S.rows[q], arity,
                                                                 keep);
         SRDL_CHECK_LAUNCH();
     }
