@@ -16,6 +16,7 @@ namespace srdl {
 
 constexpr int kMI = 4;                 // outputs per thread
 constexpr int kMT = kThreads * kMI;    // outputs per block tile (1024)
+constexpr int kMTS = kMT + 1;          // tile stride: + one B sentinel past the tile
 
 // Rows of a segment read as packed keys (same layout as the staged keys).
 struct PackedRows {
@@ -56,17 +57,19 @@ __device__ __forceinline__ void tile_bounds(uint64_t na, uint64_t nb, const LE &
     __syncthreads();
 }
 
-// smem layout for row tiles: column c of tile row k at s[c * kMT + k];
-// A rows at [0, ta), B rows at [ta, ta + tb)
+// smem layout for row tiles: column c of tile row k at s[c * kMTS + k];
+// A rows at [0, ta), B rows at [ta, ta + tb), and for the anti-join the B
+// row following the tile at ta + tb (a staged row equal to it is the last A
+// element before the tile boundary and must still be recognised)
 __device__ __forceinline__ int smem_row_cmp(const uint32_t *s, uint32_t x, uint32_t y, uint32_t arity) {
     for (uint32_t c = 0; c < arity; ++c) {
-        const uint32_t u = s[c * kMT + x], v = s[c * kMT + y];
+        const uint32_t u = s[c * kMTS + x], v = s[c * kMTS + y];
         if (u != v) return u < v ? -1 : 1;
     }
     return 0;
 }
 
-// Merge two sorted row sets (ties: A first) into out. Dynamic smem: arity*kMT*4.
+// Merge two sorted row sets (ties: A first) into out. Dynamic smem: arity*kMTS*4.
 static __global__ void __launch_bounds__(kThreads)
     mp_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, MutCols out) {
     extern __shared__ uint32_t tile[];
@@ -78,7 +81,7 @@ static __global__ void __launch_bounds__(kThreads)
     const uint64_t b0 = d0 - a0;
     for (uint32_t c = 0; c < arity; ++c) {
         for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads)
-            tile[c * kMT + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
+            tile[c * kMTS + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
     }
     __syncthreads();
     const uint32_t k0 = threadIdx.x * kMI;
@@ -97,7 +100,7 @@ static __global__ void __launch_bounds__(kThreads)
     for (uint32_t k = k0; k < kend; ++k) {
         const bool take_a = j >= tb || (i < ta && smem_row_cmp(tile, i, ta + j, arity) <= 0);
         const uint32_t src = take_a ? i++ : ta + j++;
-        for (uint32_t c = 0; c < arity; ++c) out.c[c][d0 + k] = tile[c * kMT + src];
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][d0 + k] = tile[c * kMTS + src];
     }
 }
 
@@ -105,14 +108,21 @@ static __global__ void __launch_bounds__(kThreads)
 static __global__ void __launch_bounds__(kThreads)
     mp_diff_keys(const uint64_t *__restrict__ keys, uint64_t na, PackedRows B, uint64_t nb,
                  uint32_t *__restrict__ keep) {
-    __shared__ uint64_t tile[kMT];
+    __shared__ uint64_t tile[kMTS];
     __shared__ uint64_t sh[4];
     auto le = [&](uint64_t i, uint64_t j) { return keys[i] <= B[j]; };
     tile_bounds(na, nb, le, sh);
     const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
     const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
     const uint64_t b0 = d0 - a0;
-    for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads) tile[k] = k < ta ? keys[a0 + k] : B[b0 + k - ta];
+    for (uint32_t k = threadIdx.x; k <= ta + tb; k += kThreads) {
+        if (k < ta)
+            tile[k] = keys[a0 + k];
+        else if (k < ta + tb || b0 + tb < nb)
+            tile[k] = B[b0 + k - ta];  // k == ta + tb: sentinel B row after the tile
+        else
+            tile[k] = ~0ull;
+    }
     __syncthreads();
     const uint32_t k0 = threadIdx.x * kMI;
     if (k0 >= ta + tb) return;
@@ -128,7 +138,7 @@ static __global__ void __launch_bounds__(kThreads)
     const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
     for (uint32_t k = k0; k < kend; ++k) {
         if (i < ta && (j >= tb || tile[i] <= tile[ta + j])) {
-            if (j < tb && tile[i] == tile[ta + j]) keep[a0 + i] = 0;
+            if (tile[i] == tile[ta + j]) keep[a0 + i] = 0;  // j <= tb: sentinel included
             ++i;
         } else {
             ++j;
@@ -137,7 +147,7 @@ static __global__ void __launch_bounds__(kThreads)
 }
 
 // keep[i] = 0 for every staged row of A present in segment B (row compare).
-// Dynamic smem: arity*kMT*4.
+// Dynamic smem: arity*kMTS*4.
 static __global__ void __launch_bounds__(kThreads)
     mp_diff_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, uint32_t *__restrict__ keep) {
     extern __shared__ uint32_t tile[];
@@ -147,9 +157,10 @@ static __global__ void __launch_bounds__(kThreads)
     const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
     const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
     const uint64_t b0 = d0 - a0;
+    const bool sentinel = b0 + tb < nb;
     for (uint32_t c = 0; c < arity; ++c) {
-        for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads)
-            tile[c * kMT + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
+        for (uint32_t k = threadIdx.x; k < ta + tb + (sentinel ? 1u : 0u); k += kThreads)
+            tile[c * kMTS + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
     }
     __syncthreads();
     const uint32_t k0 = threadIdx.x * kMI;
@@ -165,9 +176,10 @@ static __global__ void __launch_bounds__(kThreads)
     uint32_t i = lo, j = k0 - lo;
     const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
     for (uint32_t k = k0; k < kend; ++k) {
-        const int c = (i < ta && j < tb) ? smem_row_cmp(tile, i, ta + j, arity) : (i < ta ? -1 : 1);
-        if (c <= 0) {
-            if (c == 0) keep[a0 + i] = 0;
+        if (i < ta && (j >= tb || smem_row_cmp(tile, i, ta + j, arity) <= 0)) {
+            // A step: member if equal to the current B row (j == tb is the
+            // sentinel row after the tile, when there is one)
+            if ((j < tb || sentinel) && smem_row_cmp(tile, i, ta + j, arity) == 0) keep[a0 + i] = 0;
             ++i;
         } else {
             ++j;
@@ -176,6 +188,6 @@ static __global__ void __launch_bounds__(kThreads)
 }
 
 inline unsigned mp_grid(uint64_t n) { return grid_for(n, kMT); }
-inline size_t mp_smem(uint32_t arity) { return (size_t)arity * kMT * sizeof(uint32_t); }
+inline size_t mp_smem(uint32_t arity) { return (size_t)arity * kMTS * sizeof(uint32_t); }
 
 }  // namespace srdl

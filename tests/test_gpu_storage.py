@@ -137,3 +137,19 @@ def test_compute_delta_chunked_equals_single(dev, monkeypatch):
     assert torch.equal(whole, chunked)
     want = ost.compute_delta(host(staged), np.empty((0, 2), np.int64), full_rows)
     assert np.array_equal(host(chunked), want)
+
+
+@pytest.mark.parametrize("arity,bits", [(1, 21), (2, 12), (3, 32)])  # 3x32 bits: row-compare path
+def test_anti_join_and_merge_across_tile_boundaries(dev, arity, bits):
+    """Every staged row equal to a full row must be recognised even when the
+    pair straddles a merge-path tile boundary (1024 outputs per tile)."""
+    rng = np.random.default_rng(arity)
+    top = min(1 << bits, 1 << 20)
+    full = ost.sort_dedup(rng.integers(0, top, size=(300_000, arity)))
+    extra = ost.difference(ost.sort_dedup(rng.integers(0, top, size=(50_000, arity))), full)
+    staged = np.concatenate([full, full[::3], extra])
+    got = dev.compute_delta(to_dev(staged, arity), [to_dev(full, arity)], bits)
+    assert np.array_equal(host(got), extra)
+    # interleaved disjoint halves merge back to the whole
+    a, b = full[0::2], full[1::2]
+    assert np.array_equal(host(dev.merge(to_dev(a, arity), to_dev(b, arity))), full)
