@@ -180,9 +180,26 @@ class Recursive(Workload):
         dt = time.perf_counter() - t0
         n = len(rels[self.output])
         edb_n = sum(len(v) for v in edb.values())
+        self.oracle_rows = rels[self.output]
+        self.sample_facts = facts
         return n, dt, (f"full fixpoint of a scaled-down instance of the same generator "
                        f"({edb_n} EDB facts -> {n} {self.output} tuples in {dt:.2f} s), numpy "
                        "semi-naive generic-join restatement of the reference")
+
+    def parity(self):
+        """Engine fixpoint on the sampled instance vs the oracle's (bit-exact)."""
+        import torch
+
+        from paper_2604_20073_b200 import Engine, parse
+        from paper_2604_20073_b200 import device as dev
+
+        eng = Engine(parse(self.program), schedule="stream")
+        for k, v in self.sample_facts.items():
+            eng.load_columns(k, torch.from_numpy(v).to(dev.device()))
+        eng.solve()
+        got = eng.relation_columns(self.output).cpu().numpy().astype(np.int64).T
+        return {"checked": "full fixpoint of the sampled instance vs the CPU oracle",
+                "rows": int(len(self.oracle_rows)), "match": bool(np.array_equal(got, self.oracle_rows))}
 
 
 WORKLOADS = {"triangle": TriangleRMAT, "tc": "tc", "sg": "sg", "andersen": "andersen"}
@@ -466,6 +483,8 @@ def cpu_sample(wl, inputs_host, target_s=12.0, seed=0):
         out = join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=sample, cache=cache)
         dt = time.perf_counter() - t0
         if dt > target_s / 4 or take >= len(roots):
+            wl.sample_roots = sample
+            wl.oracle_rows = np.unique(out, axis=0) if len(out) else out
             return len(out), dt, take, len(roots)
         take = min(len(roots), int(take * max(2.0, target_s / max(dt, 1e-3) / 2)))
 
@@ -479,6 +498,38 @@ def cpu_baseline(wl, inputs):
     else:
         n, dt, sample = wl.cpu_sample()
     return {"value": n / dt, "unit": "tuples/s", "cores": 1, "kind": "port", "sample": sample}
+
+
+def triangle_parity(wl, gpu_rows):
+    """GPU output restricted to the sampled root keys vs the oracle's rows."""
+    import torch
+
+    x = gpu_rows[0].view(torch.int32).to(torch.int64)
+    keys = torch.from_numpy(np.asarray(wl.sample_roots, dtype=np.int64)).to(x.device)
+    sel = torch.isin(x, keys)
+    got = gpu_rows.view(torch.int32)[:, sel].to(torch.int64).cpu().numpy().T
+    got = got[np.lexsort(got.T[::-1])] if len(got) else got
+    return {"checked": f"all output rows of {len(wl.sample_roots)} sampled root keys vs the CPU oracle",
+            "rows": int(len(wl.oracle_rows)), "match": bool(np.array_equal(got, wl.oracle_rows)),
+            "sorted_unique": True}
+
+
+def parity_check(wl, inputs):
+    """Bit-exact comparison of one more device evaluation with the oracle on
+    the sample the CPU baseline used (not timed)."""
+    from paper_2604_20073_b200 import Engine, parse
+    from paper_2604_20073_b200 import device as dev
+
+    if not isinstance(wl, TriangleRMAT):
+        return wl.parity()
+    eng = Engine(parse(wl.program), schedule="stream")
+    for k, v in inputs.items():
+        eng.load_columns(k, v)
+    eng.solve()
+    rows = eng.relation_columns(wl.output)
+    out = triangle_parity(wl, rows)
+    out["sorted_unique"] = bool(dev.is_sorted_strict(rows))
+    return out
 
 
 def bench_reference(args, rank, world):
@@ -560,6 +611,7 @@ def main():
     result, wl, inputs = bench_ours(args, rank, world, dist)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(wl, inputs)
+        result["parity"] = parity_check(wl, inputs)
     if dist:
         dist.destroy_process_group()
     if rank == 0:

@@ -43,16 +43,35 @@ __device__ __forceinline__ uint64_t mp_split(uint64_t d, uint64_t na, uint64_t n
     return lo;
 }
 
-// Tile bounds: a0/a1 in A for this block's diagonal range (thread 0, smem).
+// Tile splits for every block, computed by a separate fully parallel
+// kernel (one thread per tile boundary): splits[t] = A elements among the
+// first t*kMT outputs, t in [0, tiles].
 template <class LE>
-__device__ __forceinline__ void tile_bounds(uint64_t na, uint64_t nb, const LE &le, uint64_t *sh) {
+__device__ __forceinline__ void split_all(uint64_t na, uint64_t nb, const LE &le, uint64_t *splits) {
+    const uint64_t n = na + nb, tiles = (n + kMT - 1) / kMT;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= tiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = t * kMT < n ? t * kMT : n;
+        splits[t] = mp_split(d, na, nb, le);
+    }
+}
+
+static __global__ void mp_splits_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity,
+                                      uint64_t *splits) {
+    split_all(na, nb, [&](uint64_t i, uint64_t j) { return row_cmp(A, i, B, j, arity) <= 0; }, splits);
+}
+
+
+
+// Tile bounds of this block from the precomputed splits.
+__device__ __forceinline__ void tile_bounds(uint64_t na, uint64_t nb, const uint64_t *splits,
+                                            uint64_t *sh) {
     if (threadIdx.x == 0) {
         const uint64_t n = na + nb, d0 = (uint64_t)blockIdx.x * kMT;
-        const uint64_t d1 = d0 + kMT < n ? d0 + kMT : n;
-        sh[0] = mp_split(d0, na, nb, le);
-        sh[1] = mp_split(d1, na, nb, le);
+        sh[0] = splits[blockIdx.x];
+        sh[1] = splits[blockIdx.x + 1];
         sh[2] = d0;
-        sh[3] = d1;
+        sh[3] = d0 + kMT < n ? d0 + kMT : n;
     }
     __syncthreads();
 }
@@ -71,11 +90,11 @@ __device__ __forceinline__ int smem_row_cmp(const uint32_t *s, uint32_t x, uint3
 
 // Merge two sorted row sets (ties: A first) into out. Dynamic smem: arity*kMTS*4.
 static __global__ void __launch_bounds__(kThreads)
-    mp_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, MutCols out) {
+    mp_merge_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, const uint64_t *splits,
+                  MutCols out) {
     extern __shared__ uint32_t tile[];
     __shared__ uint64_t sh[4];
-    auto le = [&](uint64_t i, uint64_t j) { return row_cmp(A, i, B, j, arity) <= 0; };
-    tile_bounds(na, nb, le, sh);
+    tile_bounds(na, nb, splits, sh);
     const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
     const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
     const uint64_t b0 = d0 - a0;
@@ -107,11 +126,10 @@ static __global__ void __launch_bounds__(kThreads)
 // keep[i] = 0 for every staged key present in the packed segment B.
 static __global__ void __launch_bounds__(kThreads)
     mp_diff_keys(const uint64_t *__restrict__ keys, uint64_t na, PackedRows B, uint64_t nb,
-                 uint32_t *__restrict__ keep) {
+                 const uint64_t *splits, uint32_t *__restrict__ keep) {
     __shared__ uint64_t tile[kMTS];
     __shared__ uint64_t sh[4];
-    auto le = [&](uint64_t i, uint64_t j) { return keys[i] <= B[j]; };
-    tile_bounds(na, nb, le, sh);
+    tile_bounds(na, nb, splits, sh);
     const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
     const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
     const uint64_t b0 = d0 - a0;
@@ -149,11 +167,11 @@ static __global__ void __launch_bounds__(kThreads)
 // keep[i] = 0 for every staged row of A present in segment B (row compare).
 // Dynamic smem: arity*kMTS*4.
 static __global__ void __launch_bounds__(kThreads)
-    mp_diff_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, uint32_t *__restrict__ keep) {
+    mp_diff_rows(Cols A, uint64_t na, Cols B, uint64_t nb, uint32_t arity, const uint64_t *splits,
+                 uint32_t *__restrict__ keep) {
     extern __shared__ uint32_t tile[];
     __shared__ uint64_t sh[4];
-    auto le = [&](uint64_t i, uint64_t j) { return row_cmp(A, i, B, j, arity) <= 0; };
-    tile_bounds(na, nb, le, sh);
+    tile_bounds(na, nb, splits, sh);
     const uint64_t a0 = sh[0], a1 = sh[1], d0 = sh[2], d1 = sh[3];
     const uint32_t ta = (uint32_t)(a1 - a0), tb = (uint32_t)((d1 - d0) - ta);
     const uint64_t b0 = d0 - a0;
@@ -187,7 +205,13 @@ static __global__ void __launch_bounds__(kThreads)
     }
 }
 
+static __global__ void mp_splits_keys(const uint64_t *__restrict__ keys, uint64_t na, PackedRows B,
+                                      uint64_t nb, uint64_t *splits) {
+    split_all(na, nb, [&](uint64_t i, uint64_t j) { return keys[i] <= B[j]; }, splits);
+}
+
 inline unsigned mp_grid(uint64_t n) { return grid_for(n, kMT); }
+inline uint64_t mp_tiles(uint64_t n) { return (n + kMT - 1) / kMT; }
 inline size_t mp_smem(uint32_t arity) { return (size_t)arity * kMTS * sizeof(uint32_t); }
 
 }  // namespace srdl

@@ -243,7 +243,12 @@ int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, 
         cudaStream_t s = (cudaStream_t)stream;
         Cols A = na ? make_cols(a, arity) : Cols{};
         Cols B = nb ? make_cols(b, arity) : Cols{};
-        mp_merge_rows<<<mp_grid(n), kThreads, mp_smem(arity), s>>>(A, na, B, nb, arity, make_mut(out, arity));
+        Scratch splits((mp_tiles(n) + 1) * sizeof(uint64_t), s);
+        mp_splits_rows<<<stride_grid(mp_tiles(n) + 1), kThreads, 0, s>>>(A, na, B, nb, arity,
+                                                                        splits.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        mp_merge_rows<<<mp_grid(n), kThreads, mp_smem(arity), s>>>(A, na, B, nb, arity,
+                                                                   splits.as<uint64_t>(), make_mut(out, arity));
         SRDL_CHECK_LAUNCH();
     });
 }

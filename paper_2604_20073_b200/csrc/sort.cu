@@ -198,11 +198,51 @@ __global__ void flag_rows(Cols rows, uint64_t n, uint32_t arity, uint32_t *__res
         keep[i] = (i == 0) || row_cmp(rows, i - 1, rows, i, arity) != 0;
 }
 
+// Per-row binary search anti-join, for a small staged set against a large
+// segment (the merge path would stream the whole segment).
+__global__ void bs_diff_keys(const uint64_t *__restrict__ keys, uint64_t n, PackedRows B, uint64_t nb,
+                             uint32_t *__restrict__ keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!keep[i]) continue;
+        const uint64_t k = keys[i];
+        uint64_t lo = 0, hi = nb;
+        while (lo < hi) {
+            uint64_t mid = lo + ((hi - lo) >> 1);
+            if (B[mid] < k) lo = mid + 1; else hi = mid;
+        }
+        if (lo < nb && B[lo] == k) keep[i] = 0;
+    }
+}
+
+__global__ void bs_diff_rows(Cols A, uint64_t n, Cols B, uint64_t nb, uint32_t arity,
+                             uint32_t *__restrict__ keep) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!keep[i]) continue;
+        const uint64_t pos = row_bound(B, 0, nb, A, i, arity, false);
+        if (pos < nb && row_cmp(B, pos, A, i, arity) == 0) keep[i] = 0;
+    }
+}
+
+// binary search when the segment is this many times larger than the staged set
+constexpr uint64_t kSearchRatio = 24;
+
 static void anti_join_keys(const uint64_t *keys, uint64_t n, const Segs &S, uint32_t arity,
                            uint32_t bits, uint32_t *keep, cudaStream_t s) {
     for (uint32_t q = 0; q < S.nseg; ++q) {
         PackedRows B{S.seg[q], arity, bits};
-        mp_diff_keys<<<mp_grid(n + S.rows[q]), kThreads, 0, s>>>(keys, n, B, S.rows[q], keep);
+        if (S.rows[q] > kSearchRatio * n) {
+            bs_diff_keys<<<stride_grid(n), kThreads, 0, s>>>(keys, n, B, S.rows[q], keep);
+            SRDL_CHECK_LAUNCH();
+            continue;
+        }
+        const uint64_t m = n + S.rows[q];
+        Scratch splits((mp_tiles(m) + 1) * sizeof(uint64_t), s);
+        mp_splits_keys<<<stride_grid(mp_tiles(m) + 1), kThreads, 0, s>>>(keys, n, B, S.rows[q],
+                                                                        splits.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        mp_diff_keys<<<mp_grid(m), kThreads, 0, s>>>(keys, n, B, S.rows[q], splits.as<uint64_t>(), keep);
         SRDL_CHECK_LAUNCH();
     }
 }
@@ -210,8 +250,18 @@ static void anti_join_keys(const uint64_t *keys, uint64_t n, const Segs &S, uint
 static void anti_join_rows(const Cols &rows, uint64_t n, const Segs &S, uint32_t arity,
                            uint32_t *keep, cudaStream_t s) {
     for (uint32_t q = 0; q < S.nseg; ++q) {
-        mp_diff_rows<<<mp_grid(n + S.rows[q]), kThreads, mp_smem(arity), s>>>(rows, n, S.seg[q], S.rows[q], arity,
-                                                                keep);
+        if (S.rows[q] > kSearchRatio * n) {
+            bs_diff_rows<<<stride_grid(n), kThreads, 0, s>>>(rows, n, S.seg[q], S.rows[q], arity, keep);
+            SRDL_CHECK_LAUNCH();
+            continue;
+        }
+        const uint64_t m = n + S.rows[q];
+        Scratch splits((mp_tiles(m) + 1) * sizeof(uint64_t), s);
+        mp_splits_rows<<<stride_grid(mp_tiles(m) + 1), kThreads, 0, s>>>(rows, n, S.seg[q], S.rows[q],
+                                                                        arity, splits.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        mp_diff_rows<<<mp_grid(m), kThreads, mp_smem(arity), s>>>(rows, n, S.seg[q], S.rows[q], arity,
+                                                                  splits.as<uint64_t>(), keep);
         SRDL_CHECK_LAUNCH();
     }
 }

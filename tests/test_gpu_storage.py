@@ -153,3 +153,18 @@ def test_anti_join_and_merge_across_tile_boundaries(dev, arity, bits):
     # interleaved disjoint halves merge back to the whole
     a, b = full[0::2], full[1::2]
     assert np.array_equal(host(dev.merge(to_dev(a, arity), to_dev(b, arity))), full)
+
+
+def test_anti_join_small_staged_vs_large_full(dev):
+    """Binary-search regime (segment > 24x staged) agrees with the oracle."""
+    rng = np.random.default_rng(23)
+    full = ost.sort_dedup(rng.integers(0, 1 << 16, size=(2_000_000, 2)))
+    staged = np.concatenate([full[rng.choice(len(full), 20_000)], rng.integers(0, 1 << 16, size=(20_000, 2))])
+    want = ost.compute_delta(staged, np.empty((0, 2), np.int64), full)
+    for bits in (16, 32):  # packed keys (2x16) and, at 2x32, still packed
+        got = dev.compute_delta(to_dev(staged, 2), [to_dev(full, 2)], bits)
+        assert np.array_equal(host(got), want)
+    full3 = np.concatenate([full, full[:, :1]], axis=1)
+    staged3 = np.concatenate([staged, staged[:, :1]], axis=1)
+    got3 = dev.compute_delta(to_dev(staged3, 3), [to_dev(full3, 3)], 32)  # row-compare path
+    assert np.array_equal(host(got3)[:, :2], want)
