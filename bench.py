@@ -30,6 +30,7 @@ the max over ranks (NCCL all-reduce on the timings only).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -344,6 +345,7 @@ def bench_ours(args, rank, world, dist):
     times = []
     with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
         for _ in range(args.steps):
+            gc.collect()  # release the previous step's engine before timing
             flush_l2(torch, flush)
             barrier()
             start = torch.cuda.Event(enable_timing=True)
@@ -364,6 +366,7 @@ def bench_ours(args, rank, world, dist):
     h2d = sum(t.numel() * 4 for t in pinned.values())
     e2e_times = []
     for i in range(max(1, min(args.steps, 3))):
+        gc.collect()
         flush_l2(torch, flush)
         barrier()
         t0 = time.perf_counter()

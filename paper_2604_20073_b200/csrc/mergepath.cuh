@@ -103,8 +103,7 @@ static __global__ void __launch_bounds__(kThreads)
             tile[c * kMTS + k] = k < ta ? __ldg(A.c[c] + a0 + k) : __ldg(B.c[c] + b0 + (k - ta));
     }
     __syncthreads();
-    const uint32_t k0 = threadIdx.x * kMI;
-    if (k0 >= ta + tb) return;
+    const uint32_t k0 = threadIdx.x * kMI < ta + tb ? threadIdx.x * kMI : ta + tb;  // idle: empty range
     // split of this thread's diagonal inside the tile
     uint32_t lo = k0 > tb ? k0 - tb : 0, hi = k0 < ta ? k0 : ta;
     while (lo < hi) {
@@ -116,10 +115,21 @@ static __global__ void __launch_bounds__(kThreads)
     }
     uint32_t i = lo, j = k0 - lo;
     const uint32_t kend = k0 + kMI < ta + tb ? k0 + kMI : ta + tb;
+    uint32_t src[kMI];
     for (uint32_t k = k0; k < kend; ++k) {
         const bool take_a = j >= tb || (i < ta && smem_row_cmp(tile, i, ta + j, arity) <= 0);
-        const uint32_t src = take_a ? i++ : ta + j++;
-        for (uint32_t c = 0; c < arity; ++c) out.c[c][d0 + k] = tile[c * kMTS + src];
+        src[k - k0] = take_a ? i++ : ta + j++;
+    }
+    // stage the merged tile column by column in shared memory (the source
+    // slots are overwritten only after every thread picked its rows), then
+    // store each column with coalesced writes
+    uint32_t vals[kMI];
+    for (uint32_t c = 0; c < arity; ++c) {
+        for (uint32_t k = k0; k < kend; ++k) vals[k - k0] = tile[c * kMTS + src[k - k0]];
+        __syncthreads();
+        for (uint32_t k = k0; k < kend; ++k) tile[c * kMTS + k] = vals[k - k0];
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < ta + tb; k += kThreads) out.c[c][d0 + k] = tile[c * kMTS + k];
     }
 }
 
