@@ -149,11 +149,18 @@ typedef struct {
     uint32_t nspec[SRDL_MAX_LEVELS];    /* atoms with columns at level L       */
     uint8_t spec[SRDL_MAX_LEVELS][SRDL_MAX_ATOMS];
     uint8_t leaf_slot[SRDL_MAX_ATOMS];  /* position in spec[depth-1] or NO_ATOM */
+    /* atoms with columns at the last two levels (depth >= 4): slot in the
+     * per-lane "mid batch" range table, or NO_ATOM; nmid = 0 disables the
+     * flattening of level depth-2 over the survivors of level depth-3 */
+    uint8_t mid_slot[SRDL_MAX_ATOMS];
+    uint32_t nmid;
     srdl_atom atom[SRDL_MAX_ATOMS];
 } srdl_plan;
 
 /* at most this many atoms may constrain the last variable of a plan */
 #define SRDL_MAX_LEAF_SPECS 6
+/* mid batching is used when at most this many atoms touch the last two levels */
+#define SRDL_MAX_MID_SPECS 8
 
 /* Root work space of one plan execution (Alg. 1 phase 1, Fig. 2).
  * The flattened units [0, T) are cut into `nslices` equal slices; launched

@@ -18,7 +18,9 @@
 //     smallest narrowed range (run starts = distinct values), every lane
 //     narrows the other sources for its own candidate by binary search, and
 //     a ballot keeps the survivors (no atomics anywhere);
-//   * levels 1..m-3 descend survivor by survivor (DFS state in shared memory);
+//   * levels 1..m-4 descend survivor by survivor (DFS state in shared memory,
+//     sized per plan); for m >= 4 the survivors of level m-3 are expanded
+//     over their level m-2 candidates in flattened chunks (mid batch);
 //   * the last two levels are flattened: the survivors of level m-2 become a
 //     batch of up to 32 parents, their leaf candidate ranges are prefix-summed
 //     across the warp and all lanes walk the concatenated ranges, so a leaf
@@ -31,6 +33,7 @@
 namespace srdl {
 
 constexpr int kJoinWarps = 4;
+constexpr int kMinBlocks = 8;  // register budget: 64K / (8 * 128) = 64 registers per thread
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kMergeMin = 64;    // shortest list length for merge-path leaves
 constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge-path
@@ -39,18 +42,86 @@ struct Rng {
     uint32_t lo, hi;
 };
 
-struct WarpState {
-    uint32_t bind[SRDL_MAX_LEVELS];
-    Rng rng[SRDL_MAX_LEVELS + 1][SRDL_MAX_ATOMS][SRDL_MAX_SEGS];  // ranges on entry of level L
-    uint32_t vals[SRDL_MAX_LEVELS][32];                           // candidates of current chunk
-    uint32_t cur[SRDL_MAX_LEVELS];                                // next driver row
-    uint32_t mask[SRDL_MAX_LEVELS];                               // survivors not yet descended
-    uint8_t drv[SRDL_MAX_LEVELS];
-    uint8_t dseg[SRDL_MAX_LEVELS];
-    Rng leaf[32][SRDL_MAX_LEAF_SPECS][SRDL_MAX_SEGS];            // per-parent leaf ranges
-    uint64_t leaf_pref[33];
-    uint8_t leaf_drv[32];
+// Per-warp DFS state in dynamic shared memory, sized for the plan at hand
+// (depth D, atoms A, leaf sources NL, mid-batch sources NM) so small plans
+// do not pay for the worst-case footprint.
+struct View {
+    uint64_t *leaf_pref;  // [33] exclusive prefix of parent leaf lengths
+    uint64_t *mid_pref;   // [33] exclusive prefix of grandparent candidate lengths
+    Rng *rng;             // [(D+1) * A * 2] ranges on entry of level L
+    Rng *leaf;            // [32 * NL * 2] per-parent leaf ranges
+    Rng *mid;             // [32 * NM * 2] per-grandparent ranges of deep atoms
+    uint32_t *vals;       // [D * 32] candidates of the current chunk per level
+    uint32_t *bind;       // [D] bound values (serial DFS levels)
+    uint32_t *cur;        // [D] next driver row per level
+    uint32_t *mask;       // [D] survivors not yet descended
+    uint8_t *drv, *dseg;  // [D] driver atom and segment per level
+    uint8_t *leaf_drv;    // [32]
+    uint8_t *mid_drv;     // [32]
+    uint8_t *gp;          // [32] grandparent lane of each mid-batch parent
+    uint32_t *gp_active;  // [1] parents come from a mid batch
+    uint32_t A, NL, NM;
+
+    __device__ __forceinline__ Rng &R(int L, uint32_t a, uint32_t s) const {
+        return rng[((L * A + a) << 1) + s];
+    }
+    __device__ __forceinline__ Rng &LF(uint32_t p, uint32_t j, uint32_t s) const {
+        return leaf[((p * NL + j) << 1) + s];
+    }
+    __device__ __forceinline__ Rng &MD(uint32_t g, uint32_t j, uint32_t s) const {
+        return mid[((g * NM + j) << 1) + s];
+    }
+    __device__ __forceinline__ uint32_t &V(int L, uint32_t lane) const { return vals[L * 32 + lane]; }
 };
+
+__host__ __device__ inline size_t warp_bytes(uint32_t D, uint32_t A, uint32_t NL, uint32_t NM) {
+    size_t b = 2 * 33 * 8;                          // prefixes
+    b += (size_t)(D + 1) * A * 2 * sizeof(Rng);     // rng
+    b += (size_t)32 * NL * 2 * sizeof(Rng);         // leaf
+    b += (size_t)32 * NM * 2 * sizeof(Rng);         // mid
+    b += (size_t)D * 32 * 4 + (size_t)3 * D * 4;    // vals, bind, cur, mask
+    b += (size_t)2 * D + 3 * 32 + 4;                // drv, dseg, leaf_drv, mid_drv, gp, flag
+    return (b + 15) & ~(size_t)15;
+}
+
+__device__ __forceinline__ View make_view(unsigned char *base, uint32_t D, uint32_t A, uint32_t NL,
+                                          uint32_t NM) {
+    View v;
+    v.A = A;
+    v.NL = NL;
+    v.NM = NM;
+    unsigned char *p = base;
+    v.leaf_pref = (uint64_t *)p;
+    p += 33 * 8;
+    v.mid_pref = (uint64_t *)p;
+    p += 33 * 8;
+    v.rng = (Rng *)p;
+    p += (size_t)(D + 1) * A * 2 * sizeof(Rng);
+    v.leaf = (Rng *)p;
+    p += (size_t)32 * NL * 2 * sizeof(Rng);
+    v.mid = (Rng *)p;
+    p += (size_t)32 * NM * 2 * sizeof(Rng);
+    v.vals = (uint32_t *)p;
+    p += (size_t)D * 32 * 4;
+    v.bind = (uint32_t *)p;
+    p += D * 4;
+    v.cur = (uint32_t *)p;
+    p += D * 4;
+    v.mask = (uint32_t *)p;
+    p += D * 4;
+    v.gp_active = (uint32_t *)p;
+    p += 4;
+    v.drv = p;
+    p += D;
+    v.dseg = p;
+    p += D;
+    v.leaf_drv = p;
+    p += 32;
+    v.mid_drv = p;
+    p += 32;
+    v.gp = p;
+    return v;
+}
 
 __device__ __forceinline__ uint32_t lbound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
                                            uint32_t v) {
@@ -147,9 +218,9 @@ __device__ __forceinline__ uint32_t narrow_first(const srdl_atom &A, int s, int 
 
 template <bool WRITE>
 struct Sink {
-    uint64_t n;       // tuples emitted so far by this warp (uniform)
-    uint64_t base;    // write offset of this warp (materialize)
-    __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const WarpState &S,
+    uint64_t n;       // tuples emitted so far in this slice (uniform)
+    uint64_t base;    // write offset of this slice (materialize)
+    __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const View &S,
                                          bool alive, uint32_t parent, uint32_t v, int leaf) {
         const uint32_t m = __ballot_sync(kFull, alive);
         if (WRITE && alive) {
@@ -162,7 +233,9 @@ struct Sink {
                 else if (lvl == leaf)
                     val = v;
                 else if (lvl == leaf - 1)
-                    val = S.vals[leaf - 1][parent];
+                    val = S.V(leaf - 1, parent);
+                else if (lvl == leaf - 2 && *S.gp_active)
+                    val = S.V(leaf - 2, S.gp[parent]);
                 else
                     val = S.bind[lvl];
                 X.out[h][pos] = val;
@@ -181,7 +254,7 @@ struct Sink {
 // comparable length, where per-element binary search would cost
 // min(a,b)*log(max(a,b)) dependent loads against (a+b)/32 coalesced steps.
 template <bool WRITE>
-__device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const WarpState &S, uint32_t p,
+__device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t p,
                            Sink<WRITE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t ja = S.leaf_drv[p], jb = 1u - ja;
@@ -189,8 +262,8 @@ __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const WarpSta
     const srdl_atom &B = P.atom[P.spec[leaf][jb]];
     const uint32_t *ca = A.seg[0].cols[A.lvl_col[leaf]];
     const uint32_t *cb = B.seg[0].cols[B.lvl_col[leaf]];
-    uint32_t ia = S.leaf[p][ja][0].lo, ea = S.leaf[p][ja][0].hi;
-    uint32_t ib = S.leaf[p][jb][0].lo, eb = S.leaf[p][jb][0].hi;
+    uint32_t ia = S.LF(p, ja, 0).lo, ea = S.LF(p, ja, 0).hi;
+    uint32_t ib = S.LF(p, jb, 0).lo, eb = S.LF(p, jb, 0).hi;
     const uint32_t l = lane_id();
     while (ia < ea && ib < eb) {
         const bool va = ia + l < ea, vb = ib + l < eb;
@@ -214,45 +287,55 @@ __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const WarpSta
     }
 }
 
-// Flattened leaf walk over the parents with len > 0 (per-lane driver range
-// lengths): prefix sum across the warp, every lane takes one (parent, row).
-template <bool WRITE>
-__device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint64_t len,
-                            Sink<WRITE> &sink) {
-    const int leaf = (int)P.depth - 1;
-    const uint32_t nls = P.nspec[leaf];
+// Owner of flat index f: last lane p with pref[p] <= f (pref nondecreasing).
+__device__ __forceinline__ uint32_t owner_of(const uint64_t *pref, uint64_t f) {
+    uint32_t lo = 0, hi = 32;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (pref[mid] <= f)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo - 1;
+}
+
+// Warp exclusive prefix of per-lane lengths into pref[0..32]; returns total.
+__device__ __forceinline__ uint64_t warp_prefix(uint64_t len, uint64_t *pref) {
     const uint32_t l = lane_id();
-    __syncwarp();
     uint64_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         uint64_t y = __shfl_up_sync(kFull, incl, o);
         if (l >= (uint32_t)o) incl += y;
     }
-    S.leaf_pref[l] = incl - len;
-    const uint64_t total = __shfl_sync(kFull, incl, 31);
-    if (l == 31) S.leaf_pref[32] = total;
     __syncwarp();
+    pref[l] = incl - len;
+    const uint64_t total = __shfl_sync(kFull, incl, 31);
+    if (l == 31) pref[32] = total;
+    __syncwarp();
+    return total;
+}
+
+// Flattened leaf walk over the parents with len > 0 (per-lane driver range
+// lengths): prefix sum across the warp, every lane takes one (parent, row).
+template <bool WRITE>
+__device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t len,
+                            Sink<WRITE> &sink) {
+    const int leaf = (int)P.depth - 1;
+    const uint32_t nls = P.nspec[leaf];
+    const uint32_t l = lane_id();
+    const uint64_t total = warp_prefix(len, S.leaf_pref);
     for (uint64_t base = 0; base < total; base += 32) {
         const uint64_t f = base + l;
         bool alive = f < total;
         uint32_t p = 0, v = 0;
         if (alive) {
-            // owner: last p with pref[p] <= f
-            uint32_t lo = 0, hi = 32;
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (S.leaf_pref[mid] <= f)
-                    lo = mid + 1;
-                else
-                    hi = mid;
-            }
-            p = lo - 1;
+            p = owner_of(S.leaf_pref, f);
             const uint32_t j = S.leaf_drv[p];
-            const uint32_t da = P.spec[leaf][j];
-            const srdl_atom &D = P.atom[da];
-            uint64_t local = f - S.leaf_pref[p];
-            const Rng r0 = S.leaf[p][j][0];
+            const srdl_atom &D = P.atom[P.spec[leaf][j]];
+            const uint64_t local = f - S.leaf_pref[p];
+            const Rng r0 = S.LF(p, j, 0);
             const uint32_t n0 = r0.hi - r0.lo;
             int s = 0;
             uint32_t row, seg_lo;
@@ -261,7 +344,7 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, WarpState &S
                 seg_lo = r0.lo;
             } else {
                 s = 1;
-                seg_lo = S.leaf[p][j][1].lo;
+                seg_lo = S.LF(p, j, 1).lo;
                 row = seg_lo + (uint32_t)(local - n0);
             }
             const uint32_t *col = D.seg[s].cols[D.lvl_col[leaf]];
@@ -276,7 +359,7 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, WarpState &S
                 if (jj == j && A.lvl_ncol[leaf] == 1) continue;
                 uint32_t tot = 0;
                 for (uint32_t q = 0; q < A.nseg; ++q) {
-                    Rng t = S.leaf[p][jj][q];
+                    Rng t = S.LF(p, jj, q);
                     if (t.lo < t.hi) tot += narrow(A, q, leaf, v, t);
                 }
                 if (A.negated ? tot != 0 : tot == 0) alive = false;
@@ -290,7 +373,7 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, WarpState &S
 // Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
 // level m-2 chunk; for m == 2 the single parent is the root rectangle).
 template <bool WRITE>
-__device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint32_t parents,
+__device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t parents,
                            Sink<WRITE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t nls = P.nspec[leaf];
@@ -310,7 +393,7 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
             const srdl_atom &A = P.atom[P.spec[leaf][j]];
             if (A.negated) continue;
             uint32_t t = 0;
-            for (uint32_t s = 0; s < A.nseg; ++s) t += S.leaf[l][j][s].hi - S.leaf[l][j][s].lo;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.LF(l, j, s).hi - S.LF(l, j, s).lo;
             if (t < best) {
                 best = t;
                 bj = j;
@@ -320,7 +403,7 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
         len = best;
         S.leaf_drv[l] = (uint8_t)bj;
         if (pairable && best >= kMergeMin && worst <= best * kMergeRatio) {
-            const Rng a1 = S.leaf[l][0][1], b1 = S.leaf[l][1][1];
+            const Rng a1 = S.LF(l, 0, 1), b1 = S.LF(l, 1, 1);
             const bool single = (P.atom[P.spec[leaf][0]].nseg < 2 || a1.lo >= a1.hi) &&
                                 (P.atom[P.spec[leaf][1]].nseg < 2 || b1.lo >= b1.hi);
             if (single) {
@@ -347,8 +430,99 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, WarpState &S,
     }
 }
 
+// Mid batch (plans of depth >= 4): the survivors of level m-3 (bit g of
+// `gps`, their deep-atom ranges in S.mid) are expanded over their level
+// m-2 candidates in flattened chunks of 32; each chunk's survivors become a
+// parent batch for the leaf. Replaces one serial descent per survivor.
+template <bool WRITE>
+__device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t gps,
+                          Sink<WRITE> &sink) {
+    const int leaf = (int)P.depth - 1, Lm = leaf - 1;
+    const uint32_t l = lane_id();
+    uint64_t len = 0;
+    if ((gps >> l) & 1u) {
+        uint32_t best = 0xffffffffu, bj = 0;
+        for (uint32_t j = 0; j < P.nspec[Lm]; ++j) {
+            const uint32_t a = P.spec[Lm][j];
+            const srdl_atom &A = P.atom[a];
+            if (A.negated) continue;
+            const uint32_t slot = P.mid_slot[a];
+            uint32_t t = 0;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.MD(l, slot, s).hi - S.MD(l, slot, s).lo;
+            if (t < best) {
+                best = t;
+                bj = j;
+            }
+        }
+        len = best;
+        S.mid_drv[l] = (uint8_t)bj;
+    }
+    const uint64_t total = warp_prefix(len, S.mid_pref);
+    if (l == 0) *S.gp_active = 1u;
+    __syncwarp();
+    for (uint64_t base = 0; base < total; base += 32) {
+        const uint64_t f = base + l;
+        bool alive = f < total;
+        uint32_t v = 0;
+        if (alive) {
+            const uint32_t g = owner_of(S.mid_pref, f);
+            const uint32_t da = P.spec[Lm][S.mid_drv[g]];
+            const srdl_atom &D = P.atom[da];
+            const uint32_t dslot = P.mid_slot[da];
+            const uint64_t local = f - S.mid_pref[g];
+            const Rng r0 = S.MD(g, dslot, 0);
+            const uint32_t n0 = r0.hi - r0.lo;
+            int s = 0;
+            uint32_t row, seg_lo;
+            if (local < n0) {
+                row = r0.lo + (uint32_t)local;
+                seg_lo = r0.lo;
+            } else {
+                s = 1;
+                seg_lo = S.MD(g, dslot, 1).lo;
+                row = seg_lo + (uint32_t)(local - n0);
+            }
+            const uint32_t *col = D.seg[s].cols[D.lvl_col[Lm]];
+            v = __ldg(col + row);
+            alive = row == seg_lo || __ldg(col + row - 1) != v;
+            if (alive && s == 1 && n0) {
+                Rng t = r0;
+                alive = narrow_first(D, 0, Lm, v, t) == 0;
+            }
+            for (uint32_t j = 0; j < P.nspec[Lm] && alive; ++j) {
+                const uint32_t b = P.spec[Lm][j];
+                const srdl_atom &A = P.atom[b];
+                const uint32_t slot = P.mid_slot[b], ls = P.leaf_slot[b];
+                uint32_t tot = 0;
+                for (uint32_t q = 0; q < A.nseg; ++q) {
+                    Rng t = S.MD(g, slot, q);
+                    if (t.lo < t.hi) tot += narrow(A, q, Lm, v, t);
+                    else t.hi = t.lo;
+                    if (ls != SRDL_NO_ATOM) S.LF(l, ls, q) = t;
+                }
+                if (A.negated ? (A.check_level == Lm && tot != 0) : tot == 0) alive = false;
+            }
+            if (alive) {
+                for (uint32_t j = 0; j < P.nspec[leaf]; ++j) {
+                    const uint32_t b = P.spec[leaf][j];
+                    if (P.atom[b].lvl_ncol[Lm]) continue;
+                    for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.LF(l, j, q) = S.MD(g, P.mid_slot[b], q);
+                }
+                S.gp[l] = (uint8_t)g;
+            }
+            S.V(Lm, l) = v;
+        }
+        const uint32_t m = __ballot_sync(kFull, alive);
+        __syncwarp();
+        if (m) leaf_batch<WRITE>(P, X, S, m, sink);
+    }
+    __syncwarp();
+    if (l == 0) *S.gp_active = 0u;
+    __syncwarp();
+}
+
 // Pick the smallest candidate source of level L and reset the chunk cursor.
-__device__ __forceinline__ void open_level(const srdl_plan &P, WarpState &S, int L) {
+__device__ __forceinline__ void open_level(const srdl_plan &P, const View &S, int L) {
     if (lane_id() == 0) {
         uint32_t best = 0xffffffffu, ba = 0;
         for (uint32_t j = 0; j < P.nspec[L]; ++j) {
@@ -356,7 +530,7 @@ __device__ __forceinline__ void open_level(const srdl_plan &P, WarpState &S, int
             const srdl_atom &A = P.atom[a];
             if (A.negated) continue;
             uint32_t t = 0;
-            for (uint32_t s = 0; s < A.nseg; ++s) t += S.rng[L][a][s].hi - S.rng[L][a][s].lo;
+            for (uint32_t s = 0; s < A.nseg; ++s) t += S.R(L, a, s).hi - S.R(L, a, s).lo;
             if (t < best) {
                 best = t;
                 ba = a;
@@ -364,7 +538,7 @@ __device__ __forceinline__ void open_level(const srdl_plan &P, WarpState &S, int
         }
         S.drv[L] = (uint8_t)ba;
         S.dseg[L] = 0;
-        S.cur[L] = S.rng[L][ba][0].lo;
+        S.cur[L] = S.R(L, ba, 0).lo;
         S.mask[L] = 0;
     }
     __syncwarp();
@@ -372,7 +546,7 @@ __device__ __forceinline__ void open_level(const srdl_plan &P, WarpState &S, int
 
 // Next 32 driver rows of level L -> filtered candidates. False when exhausted.
 template <bool WRITE>
-__device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, WarpState &S, int L,
+__device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S, int L,
                            Sink<WRITE> &sink) {
     const uint32_t l = lane_id();
     const uint32_t a = S.drv[L];
@@ -381,11 +555,11 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, WarpState &S,
     uint32_t r = S.cur[L];
     while (true) {
         if (s >= D.nseg) return false;
-        if (r < S.rng[L][a][s].hi) break;
+        if (r < S.R(L, a, s).hi) break;
         ++s;
-        if (s < D.nseg) r = S.rng[L][a][s].lo;
+        if (s < D.nseg) r = S.R(L, a, s).lo;
     }
-    const Rng seg = S.rng[L][a][s];
+    const Rng seg = S.R(L, a, s);
     const uint32_t row = r + l;
     const uint32_t *col = D.seg[s].cols[D.lvl_col[L]];
     bool alive = row < seg.hi;
@@ -395,23 +569,29 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, WarpState &S,
         alive = row == seg.lo || __ldg(col + row - 1) != v;
     }
     if (alive && s == 1) {
-        Rng t = S.rng[L][a][0];
+        Rng t = S.R(L, a, 0);
         if (t.lo < t.hi) alive = narrow_first(D, 0, L, v, t) == 0;
     }
     const int leaf = (int)P.depth - 1;
     const bool parents_level = L == leaf - 1;
+    const bool gp_level = P.nmid && L == leaf - 2;
     for (uint32_t j = 0; j < P.nspec[L] && alive; ++j) {
         const uint32_t b = P.spec[L][j];
         const srdl_atom &A = P.atom[b];
-        const uint32_t slot = P.leaf_slot[b];
-        const bool keep = parents_level && slot != SRDL_NO_ATOM;
-        if (b == a && A.lvl_ncol[L] == 1 && !keep && A.nseg == 1) continue;
+        const uint32_t slot = parents_level ? P.leaf_slot[b] : (gp_level ? P.mid_slot[b] : SRDL_NO_ATOM);
+        const bool keep = slot != SRDL_NO_ATOM;
+        if (b == a && A.lvl_ncol[L] == 1 && !keep) continue;
         uint32_t tot = 0;
         for (uint32_t q = 0; q < A.nseg; ++q) {
-            Rng t = S.rng[L][b][q];
+            Rng t = S.R(L, b, q);
             if (t.lo < t.hi) tot += narrow(A, q, L, v, t);
             else t.hi = t.lo;
-            if (keep) S.leaf[l][slot][q] = t;
+            if (keep) {
+                if (parents_level)
+                    S.LF(l, slot, q) = t;
+                else
+                    S.MD(l, slot, q) = t;
+            }
         }
         if (A.negated ? (A.check_level == L && tot != 0) : tot == 0) alive = false;
     }
@@ -420,39 +600,48 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, WarpState &S,
         for (uint32_t j = 0; j < P.nspec[leaf]; ++j) {
             const uint32_t b = P.spec[leaf][j];
             if (P.atom[b].lvl_ncol[L]) continue;
-            for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.leaf[l][j][q] = S.rng[L][b][q];
+            for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.LF(l, j, q) = S.R(L, b, q);
         }
     }
-    S.vals[L][l] = v;
+    if (gp_level && alive) {
+        // deep sources not constrained at this level keep their ranges
+        for (uint32_t b = 0; b < P.natoms; ++b) {
+            const uint32_t slot = P.mid_slot[b];
+            if (slot == SRDL_NO_ATOM || P.atom[b].lvl_ncol[L]) continue;
+            for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.MD(l, slot, q) = S.R(L, b, q);
+        }
+    }
+    S.V(L, l) = v;
     const uint32_t m = __ballot_sync(kFull, alive);
     if (l == 0) {
         S.cur[L] = seg.hi - r > 32 ? r + 32 : seg.hi;
         S.dseg[L] = (uint8_t)s;
-        S.mask[L] = parents_level ? 0u : m;
+        S.mask[L] = (parents_level || gp_level) ? 0u : m;
     }
     __syncwarp();
     if (parents_level && m) leaf_batch<WRITE>(P, X, S, m, sink);
+    if (gp_level && m) mid_batch<WRITE>(P, X, S, m, sink);
     return true;
 }
 
 // Bind survivor `ln` of level L and derive the level L+1 ranges.
-__device__ __forceinline__ void descend(const srdl_plan &P, WarpState &S, int L, uint32_t ln) {
+__device__ __forceinline__ void descend(const srdl_plan &P, const View &S, int L, uint32_t ln) {
     const uint32_t l = lane_id();
-    const uint32_t v = S.vals[L][ln];
+    const uint32_t v = S.V(L, ln);
     if (l == 0) S.bind[L] = v;
     for (uint32_t t = l; t < P.natoms * SRDL_MAX_SEGS; t += 32) {
         const uint32_t a = t / SRDL_MAX_SEGS, s = t % SRDL_MAX_SEGS;
-        Rng r = S.rng[L][a][s];
+        Rng r = S.R(L, a, s);
         const srdl_atom &A = P.atom[a];
         if (A.lvl_ncol[L] && s < A.nseg && r.lo < r.hi) narrow(A, s, L, v, r);
-        S.rng[L + 1][a][s] = r;
+        S.R(L + 1, a, s) = r;
     }
     __syncwarp();
 }
 
 // One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
 template <bool WRITE>
-__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, uint64_t k,
+__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t k,
                          uint32_t key, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
                          Sink<WRITE> &sink) {
     const uint32_t l = lane_id();
@@ -511,7 +700,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, u
     const uint32_t tot = len + __shfl_xor_sync(kFull, len, 1);
     bool dead = false;
     if (mine && s == 0 && has0) dead = A.negated ? (A.check_level == 0 && tot != 0) : tot == 0;
-    if (mine) S.rng[1][a][s] = Rng{lo, hi};
+    if (mine) S.R(1, a, s) = Rng{lo, hi};
     if (__any_sync(kFull, dead)) return;
     __syncwarp();
     if (P.depth == 1) {
@@ -520,12 +709,12 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, u
     }
     if (l == 0) {
         S.bind[0] = key;
-        S.vals[0][0] = key;
+        S.V(0, 0) = key;
     }
     if (P.depth == 2) {
         for (uint32_t t = l; t < P.nspec[1] * SRDL_MAX_SEGS; t += 32) {
             const uint32_t j = t / SRDL_MAX_SEGS, q = t % SRDL_MAX_SEGS;
-            S.leaf[0][j][q] = S.rng[1][P.spec[1][j]][q];
+            S.LF(0, j, q) = S.R(1, P.spec[1][j], q);
         }
         __syncwarp();
         leaf_batch<WRITE>(P, X, S, 1u, sink);
@@ -533,6 +722,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, u
     }
     __syncwarp();
     // DFS over levels 1..m-2; level m-2 hands its survivors to leaf_batch
+    // (and, with a mid batch, level m-3 hands its survivors to mid_batch)
     int L = 1;
     open_level(P, S, L);
     while (true) {
@@ -553,11 +743,15 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, WarpState &S, u
 }
 
 template <bool WRITE>
-__global__ void __launch_bounds__(kJoinWarps * 32)
+__global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
     wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X) {
-    __shared__ WarpState states[kJoinWarps];
+    extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t wib = threadIdx.x >> 5;
-    WarpState &S = states[wib];
+    const uint32_t NL = P.nspec[P.depth - 1] ? P.nspec[P.depth - 1] : 1;
+    const size_t wb = warp_bytes(P.depth, P.natoms, NL, P.nmid);
+    const View S = make_view(smem + wib * wb, P.depth, P.natoms, NL, P.nmid);
+    if (lane_id() == 0) *S.gp_active = 0u;
+    __syncwarp();
     const uint64_t K = X.nkeys;
     const uint64_t T = K ? X.prefix[K - 1] : 0;
     // enough slices to occupy every launched warp several times, coarser
@@ -620,6 +814,33 @@ __global__ void __launch_bounds__(kJoinWarps * 32)
     }
 }
 
+static size_t block_smem(const srdl_plan *P) {
+    const uint32_t NL = P->nspec[P->depth - 1] ? P->nspec[P->depth - 1] : 1;
+    return warp_bytes(P->depth, P->natoms, NL, P->nmid) * kJoinWarps;
+}
+
+template <bool WRITE>
+static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+    const size_t bytes = block_smem(P);
+    static bool raised = false;
+    if (!raised) {  // allow up to the full 227 KB of dynamic shared memory
+        SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<WRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       227 * 1024));
+        raised = true;
+    }
+    SRDL_REQUIRE(bytes <= 227 * 1024, "join state of %zu bytes per block exceeds shared memory", bytes);
+    // one full wave of resident blocks (the plan's shared-memory footprint and
+    // the register budget decide how many fit per SM); slices are fetched
+    // dynamically, so more blocks would only queue
+    int per_sm = 0;
+    SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<WRITE>, kJoinWarps * 32, bytes));
+    if (per_sm < 1) per_sm = 1;
+    const unsigned blocks = (unsigned)(per_sm * sm_count());
+    srdl_exec x = *X;
+    x.nwarps = blocks * kJoinWarps;
+    wcoj_kernel<WRITE><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, x);
+}
+
 static void check_plan(const srdl_plan *P, const srdl_exec *X) {
     SRDL_REQUIRE(P->depth >= 1 && P->depth <= SRDL_MAX_LEVELS, "plan depth %u unsupported", P->depth);
     SRDL_REQUIRE(P->natoms >= 1 && P->natoms <= SRDL_MAX_ATOMS, "plan has %u atoms", P->natoms);
@@ -641,10 +862,9 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
     return guarded([&] {
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
-        const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
         SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
         SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
-        wcoj_kernel<false><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
+        launch<false>(plan, ex, s);
         SRDL_CHECK_LAUNCH();
         exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
     });
@@ -654,9 +874,8 @@ int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stre
     return guarded([&] {
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
-        const unsigned blocks = (ex->nwarps + kJoinWarps - 1) / kJoinWarps;
         SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
-        wcoj_kernel<true><<<blocks, kJoinWarps * 32, 0, s>>>(*plan, *ex);
+        launch<true>(plan, ex, s);
         SRDL_CHECK_LAUNCH();
     });
 }

@@ -30,6 +30,7 @@ MAX_COLS = 8
 MAX_HEAD = 12
 MAX_SEGS = 2
 MAX_LEAF_SPECS = 6
+MAX_MID_SPECS = 8
 MAX_DIFF_SEGS = 8
 NO_ATOM = 255
 NO_SYMBOL = 0xFFFFFFFF
@@ -72,6 +73,8 @@ class PlanDesc(C.Structure):
         ("nspec", C.c_uint32 * MAX_LEVELS),
         ("spec", (C.c_uint8 * MAX_ATOMS) * MAX_LEVELS),
         ("leaf_slot", C.c_uint8 * MAX_ATOMS),
+        ("mid_slot", C.c_uint8 * MAX_ATOMS),
+        ("nmid", C.c_uint32),
         ("atom", AtomDesc * MAX_ATOMS),
     ]
 

@@ -33,7 +33,7 @@ from .faults import InternalError
 from .partition import WorkPartition, decode_workunit, encode_workunit, rectangles  # noqa: F401
 from .syntax import VAR
 
-WARPS_PER_SM = 28  # 7 resident CTAs x 4 warps (30 KB shared memory each)
+WARPS_PER_SM = 32  # slice-array sizing; the launcher picks the resident wave itself
 SLICES_PER_WARP = 256  # slice-array capacity per launched warp (fetched dynamically)
 MIN_SLICE_UNITS = 4096  # fewer, larger slices when the root space is small
 
@@ -140,6 +140,15 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                                 f"(device limit {dev.MAX_LEAF_SPECS})")
         for j, (a, _cols) in enumerate(leaf_specs):
             d.leaf_slot[a] = j
+    for a in range(dev.MAX_ATOMS):
+        d.mid_slot[a] = dev.NO_ATOM
+    if plan.depth >= 4:
+        deep = [a for a, pa in enumerate(plan.atoms)
+                if any(lvl >= plan.depth - 2 for lvl in pa.col_levels)]
+        if len(deep) <= dev.MAX_MID_SPECS:
+            for slot, a in enumerate(deep):
+                d.mid_slot[a] = slot
+            d.nmid = len(deep)
     for a, pa in enumerate(plan.atoms):
         if pa.arity > dev.MAX_COLS:
             raise InternalError(f"relation {pa.relation}: arity {pa.arity} > {dev.MAX_COLS}")
