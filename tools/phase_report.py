@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--workload", default="triangle")
     ap.add_argument("--statements", type=int, default=1_000_000)
     ap.add_argument("--schedule", default="stream")
+    ap.add_argument("--kernels", action="store_true", help="CUPTI per-kernel totals of the last run")
     args = ap.parse_args()
     if args.workload == "triangle":
         raw = dev.gen_rmat(20, 16_000_000, seed=1).view(torch.int32)
@@ -36,13 +37,28 @@ def main():
         facts = {k: torch.from_numpy(v).cuda() for k, v in gen().items()}
         program, out = suites.BASELINE_PROGRAMS[args.workload]
     for rep in range(2):
-        stats = Stats()
+        stats = Stats(enabled=not args.kernels)
         eng = Engine(parse(program), schedule=args.schedule, stats=stats)
         for k, v in facts.items():
             eng.load_columns(k, v)
+        prof = None
+        if args.kernels and rep == 1:
+            prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA])
+            prof.__enter__()
         t0 = time.perf_counter()
         summ = eng.solve()
+        torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+        if prof is not None:
+            prof.__exit__(None, None, None)
+            rows = {}
+            for ev in prof.events():
+                if ev.device_type == torch.autograd.DeviceType.CUDA:
+                    name = ev.name.split("(")[0][:60]
+                    n, t = rows.get(name, (0, 0.0))
+                    rows[name] = (n + 1, t + ev.device_time_total / 1e3)
+            top = sorted(rows.items(), key=lambda kv: -kv[1][1])[:14]
+            print(json.dumps({"kernels_ms": {k: [n, round(t, 2)] for k, (n, t) in top}}), flush=True)
         totals = {k: round(v / 1e3, 2) for k, v in sorted(stats.phase_totals().items(), key=lambda x: -x[1])}
         print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "out": summ.relations[out],
                           "iterations": [s.iterations for s in summ.strata],
