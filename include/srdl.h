@@ -204,6 +204,26 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream);
  * slices writing head tuples at slice_offsets; sets *error on divergence. */
 int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stream);
 
+/* ------------------------------------------------------------ multi-GPU
+ * Owner of a value among `world` ranks (hash partitioning of root keys):
+ * owner(v) = ((v * 2654435761) >> 8) % world, identical on host and device. */
+
+/* Stable partition of rows by the owner of column `key_col`: out holds the
+ * rows of rank 0, then rank 1, ...; counts[world] (host) the rows per rank. */
+int srdl_route_rows(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                    uint32_t world, uint32_t *const *out, uint64_t *counts, void *stream);
+
+/* Keep the rows whose column `key_col` is owned by `rank` (stable);
+ * *n_out (host) = rows kept. out has capacity n. */
+int srdl_filter_owned(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                      uint32_t world, uint32_t rank, uint32_t *const *out, uint64_t *n_out,
+                      void *stream);
+
+/* Zero the work of root keys not owned by `rank` (inclusive prefix is
+ * recomputed): every rank then enumerates only its own root keys. */
+int srdl_root_own(const uint32_t *keys, uint64_t nk, const uint32_t *odeg, const uint32_t *d2,
+                  uint32_t world, uint32_t rank, uint64_t *prefix, void *stream);
+
 /* ------------------------------------------------------------- generators
  * Synthetic inputs for the benchmarks (not on the evaluation path).
  * R-MAT edge list (Chakrabarti et al.): n = 2^scale vertices, probabilities

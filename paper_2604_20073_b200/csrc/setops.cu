@@ -175,6 +175,34 @@ __global__ void dense_offsets_kernel(const uint32_t *__restrict__ keys,
     }
 }
 
+__device__ __forceinline__ uint32_t owner_of(uint32_t v, uint32_t world) {
+    return ((uint32_t)(v * 2654435761u) >> 8) % world;
+}
+
+__global__ void owner_flags(const uint32_t *__restrict__ col, uint64_t n, uint32_t world, uint32_t rank,
+                            uint32_t *__restrict__ f) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        f[i] = owner_of(col[i], world) == rank;
+}
+
+__global__ void scatter_flagged(Cols in, uint32_t arity, const uint32_t *__restrict__ f,
+                                const uint32_t *__restrict__ pos, uint64_t n, uint64_t base, MutCols out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!f[i]) continue;
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][base + pos[i]] = __ldg(in.c[c] + i);
+    }
+}
+
+__global__ void root_own_kernel(const uint32_t *__restrict__ keys, uint64_t nk,
+                                const uint32_t *__restrict__ odeg, const uint32_t *__restrict__ d2,
+                                uint32_t world, uint32_t rank, uint64_t *__restrict__ work) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        work[i] = owner_of(keys[i], world) == rank ? (uint64_t)odeg[i] * d2[i] : 0;
+}
+
 // counter-based RNG: splitmix64 finaliser over (seed, edge, level)
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x ^= x >> 30;
@@ -331,6 +359,59 @@ int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nk
         dense_offsets_kernel<<<stride_grid((uint64_t)n_ids + 1), kThreads, 0, s>>>(keys, prefix, nkeys,
                                                                                   n_ids, off);
         SRDL_CHECK_LAUNCH();
+    });
+}
+
+// rows owned by one rank, appended at `base` of out; returns the count
+static uint64_t route_one(const Cols &in, uint32_t arity, uint64_t n, uint32_t key_col, uint32_t world,
+                          uint32_t rank, const MutCols &out, uint64_t base, cudaStream_t s) {
+    const unsigned g = stride_grid(n);
+    Scratch f(n * sizeof(uint32_t), s), pos(n * sizeof(uint32_t), s), total(sizeof(uint32_t) * 2, s);
+    owner_flags<<<g, kThreads, 0, s>>>(in.c[key_col], n, world, rank, f.as<uint32_t>());
+    SRDL_CHECK_LAUNCH();
+    exclusive_scan_u32(f.as<uint32_t>(), pos.as<uint32_t>(), n, total.as<uint32_t>(), s);
+    scatter_flagged<<<g, kThreads, 0, s>>>(in, arity, f.as<uint32_t>(), pos.as<uint32_t>(), n, base, out);
+    SRDL_CHECK_LAUNCH();
+    uint32_t cnt = 0;
+    SRDL_CUDA(cudaMemcpyAsync(&cnt, total.as<uint32_t>(), sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    SRDL_CUDA(cudaStreamSynchronize(s));
+    return cnt;
+}
+
+int srdl_route_rows(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                    uint32_t world, uint32_t *const *out, uint64_t *counts, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(world >= 1 && key_col < arity, "bad routing arguments");
+        SRDL_REQUIRE(n < (1ull << 32), "route: too many rows");
+        cudaStream_t s = (cudaStream_t)stream;
+        uint64_t base = 0;
+        for (uint32_t r = 0; r < world; ++r) {
+            counts[r] = n ? route_one(make_cols(cols, arity), arity, n, key_col, world, r,
+                                      make_mut(out, arity), base, s) : 0;
+            base += counts[r];
+        }
+    });
+}
+
+int srdl_filter_owned(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                      uint32_t world, uint32_t rank, uint32_t *const *out, uint64_t *n_out,
+                      void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(world >= 1 && rank < world && key_col < arity, "bad filter arguments");
+        SRDL_REQUIRE(n < (1ull << 32), "filter: too many rows");
+        *n_out = n ? route_one(make_cols(cols, arity), arity, n, key_col, world, rank,
+                               make_mut(out, arity), 0, (cudaStream_t)stream) : 0;
+    });
+}
+
+int srdl_root_own(const uint32_t *keys, uint64_t nk, const uint32_t *odeg, const uint32_t *d2,
+                  uint32_t world, uint32_t rank, uint64_t *prefix, void *stream) {
+    return guarded([&] {
+        if (nk == 0) return;
+        cudaStream_t s = (cudaStream_t)stream;
+        root_own_kernel<<<stride_grid(nk), kThreads, 0, s>>>(keys, nk, odeg, d2, world, rank, prefix);
+        SRDL_CHECK_LAUNCH();
+        inclusive_scan_u64(prefix, prefix, nk, s);
     });
 }
 

@@ -150,6 +150,19 @@ _SIGNATURES = {
     ),
     "srdl_wcoj_count": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
     "srdl_wcoj_materialize": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
+    "srdl_route_rows": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "srdl_filter_owned": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+         C.POINTER(C.c_uint64), C.c_void_p],
+    ),
+    "srdl_root_own": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p],
+    ),
     "srdl_gen_rmat": (
         C.c_int,
         [C.c_uint32, C.c_uint64, C.c_float, C.c_float, C.c_float, C.c_uint64, C.c_void_p,
@@ -401,6 +414,40 @@ def root_work(okeys, odeg, oprefix=None, ikeys=None, ideg=None, iprefix=None, ou
                                p(iprefix) if has_inner else None, nik, int(has_inner), d2.data_ptr(),
                                prefix.data_ptr(), p(olo), p(ilo), stream_handle()), "root_work")
     return d2, prefix, olo, ilo
+
+
+def owner(values, world: int):
+    """Host mirror of the device owner hash (numpy array or int)."""
+    import numpy as np
+
+    v = np.asarray(values, dtype=np.uint64)
+    return (((v * np.uint64(2654435761)) & np.uint64(0xFFFFFFFF)) >> np.uint64(8)) % np.uint64(world)
+
+
+def route_rows(rows: torch.Tensor, key_col: int, world: int):
+    """Rows grouped by owner rank of column key_col -> (routed rows, counts)."""
+    arity, n = rows.shape
+    out = empty_rows(arity, n)
+    counts = (C.c_uint64 * max(world, 1))()
+    check(lib().srdl_route_rows(col_ptrs(rows), arity, n, key_col, world, col_ptrs(out), counts,
+                                stream_handle()), "route_rows")
+    return out, [int(counts[r]) for r in range(world)]
+
+
+def filter_owned(rows: torch.Tensor, key_col: int, world: int, rank: int) -> torch.Tensor:
+    arity, n = rows.shape
+    out = empty_rows(arity, n)
+    got = C.c_uint64(0)
+    check(lib().srdl_filter_owned(col_ptrs(rows), arity, n, key_col, world, rank, col_ptrs(out),
+                                  C.byref(got), stream_handle()), "filter_owned")
+    return _trim(out, got.value)
+
+
+def root_own(keys, odeg, d2, prefix, world: int, rank: int):
+    """Restrict a root work prefix to the keys this rank owns (in place)."""
+    if keys.numel():
+        check(lib().srdl_root_own(keys.data_ptr(), keys.numel(), odeg.data_ptr(), d2.data_ptr(), world,
+                                  rank, prefix.data_ptr(), stream_handle()), "root_own")
 
 
 def gen_rmat(scale: int, nedges: int, a=0.57, b=0.19, c=0.19, seed=1) -> torch.Tensor:

@@ -240,7 +240,8 @@ class DevicePartition:
         return -(-t // self.slices_used()) if t else 0
 
 
-def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None, interner=None):
+def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None, interner=None,
+                    dist=None):
     if p < 1:
         raise InternalError("worker count must be >= 1")
     if prep is None:
@@ -267,6 +268,8 @@ def build_partition(plan: JoinPlan, store, p: int, prep: Prepared | None = None,
                                              outer_rows=single_outer, inner_rows=single_inner)
     else:
         d2, prefix, olo, ilo = dev.root_work(okeys, odeg, hist.prefix, outer_rows=single_outer)
+    if dist is not None and dist.world > 1:
+        dev.root_own(okeys, odeg, d2, prefix, dist.world, dist.rank)  # this rank's root keys only
     return DevicePartition(okeys, odeg, d2, prefix, p, olo, ilo)
 
 
@@ -384,11 +387,12 @@ class PlanExecution:
     """One plan's pipeline split into phases so schedulers can interleave
     the same phase of independent plans (reference executor.PlanExecution)."""
 
-    def __init__(self, plan, store, p, interner, pool=None):
+    def __init__(self, plan, store, p, interner, pool=None, dist=None):
         self.plan = plan
         self.store = store
         self.p = p
         self.interner = interner
+        self.dist = dist
         self.prep = None
         self.partition = None
         self.counts = None
@@ -399,7 +403,7 @@ class PlanExecution:
 
     def histogram(self):
         self.prep = prepare(self.plan, self.store, self.interner)
-        self.partition = build_partition(self.plan, self.store, self.p, self.prep)
+        self.partition = build_partition(self.plan, self.store, self.p, self.prep, dist=self.dist)
         return self.partition
 
     def count(self) -> CountResult:
