@@ -28,6 +28,8 @@
 //     coalesced (the paper's "adjacent threads emit adjacent positions").
 // Count and materialize run the same code (template flag WRITE), so per-warp
 // counts are exact and writes land in [offset_w, offset_w + count_w).
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace srdl {
@@ -37,6 +39,12 @@ constexpr int kMinBlocks = 8;  // register budget: 64K / (8 * 128) = 64 register
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kMergeMin = 64;    // shortest list length for merge-path leaves
 constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge-path
+
+// Launch-time specialisation derived from the plan (not part of the C ABI):
+// the kernel is instantiated per plan class so each instance carries only
+// the code paths its plans can reach (smaller code, fewer i-cache misses).
+enum Kind : int { kShallow = 0, kDepth3 = 1, kGeneral = 2 };
+
 
 struct Rng {
     uint32_t lo, hi;
@@ -545,7 +553,7 @@ __device__ __forceinline__ void open_level(const srdl_plan &P, const View &S, in
 }
 
 // Next 32 driver rows of level L -> filtered candidates. False when exhausted.
-template <bool WRITE>
+template <bool WRITE, int KIND>
 __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S, int L,
                            Sink<WRITE> &sink) {
     const uint32_t l = lane_id();
@@ -574,7 +582,7 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
     }
     const int leaf = (int)P.depth - 1;
     const bool parents_level = L == leaf - 1;
-    const bool gp_level = P.nmid && L == leaf - 2;
+    const bool gp_level = KIND == kGeneral && P.nmid && L == leaf - 2;
     for (uint32_t j = 0; j < P.nspec[L] && alive; ++j) {
         const uint32_t b = P.spec[L][j];
         const srdl_atom &A = P.atom[b];
@@ -620,7 +628,9 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
     }
     __syncwarp();
     if (parents_level && m) leaf_batch<WRITE>(P, X, S, m, sink);
-    if (gp_level && m) mid_batch<WRITE>(P, X, S, m, sink);
+    if constexpr (KIND == kGeneral) {
+        if (gp_level && m) mid_batch<WRITE>(P, X, S, m, sink);
+    }
     return true;
 }
 
@@ -640,7 +650,7 @@ __device__ __forceinline__ void descend(const srdl_plan &P, const View &S, int L
 }
 
 // One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
-template <bool WRITE>
+template <bool WRITE, int KIND>
 __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t k,
                          uint32_t key, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
                          Sink<WRITE> &sink) {
@@ -703,15 +713,15 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
     if (mine) S.R(1, a, s) = Rng{lo, hi};
     if (__any_sync(kFull, dead)) return;
     __syncwarp();
-    if (P.depth == 1) {
-        sink.emit(P, X, S, l == 0, 0, key, 0);
-        return;
-    }
     if (l == 0) {
         S.bind[0] = key;
         S.V(0, 0) = key;
     }
-    if (P.depth == 2) {
+    if (KIND == kShallow || (KIND == kGeneral && P.depth <= 2)) {
+        if (P.depth == 1) {
+            sink.emit(P, X, S, l == 0, 0, key, 0);
+            return;
+        }
         for (uint32_t t = l; t < P.nspec[1] * SRDL_MAX_SEGS; t += 32) {
             const uint32_t j = t / SRDL_MAX_SEGS, q = t % SRDL_MAX_SEGS;
             S.LF(0, j, q) = S.R(1, P.spec[1][j], q);
@@ -720,29 +730,37 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
         leaf_batch<WRITE>(P, X, S, 1u, sink);
         return;
     }
-    __syncwarp();
-    // DFS over levels 1..m-2; level m-2 hands its survivors to leaf_batch
-    // (and, with a mid batch, level m-3 hands its survivors to mid_batch)
-    int L = 1;
-    open_level(P, S, L);
-    while (true) {
-        const uint32_t m = S.mask[L];
-        if (m == 0) {
-            if (load_chunk<WRITE>(P, X, S, L, sink)) continue;
-            if (L == 1) break;
-            --L;
-            continue;
-        }
-        const uint32_t ln = __ffs(m) - 1;
+    if constexpr (KIND == kDepth3) {
+        // level 1 is the parents level: chunks of it feed leaf batches
         __syncwarp();
-        if (l == 0) S.mask[L] = m & (m - 1);
-        descend(P, S, L, ln);
-        ++L;
+        open_level(P, S, 1);
+        while (load_chunk<WRITE, KIND>(P, X, S, 1, sink)) {
+        }
+    } else if constexpr (KIND == kGeneral) {
+        __syncwarp();
+        // DFS over levels 1..m-2; level m-2 hands its survivors to leaf_batch
+        // (and, with a mid batch, level m-3 hands its survivors to mid_batch)
+        int L = 1;
         open_level(P, S, L);
+        while (true) {
+            const uint32_t m = S.mask[L];
+            if (m == 0) {
+                if (load_chunk<WRITE, KIND>(P, X, S, L, sink)) continue;
+                if (L == 1) break;
+                --L;
+                continue;
+            }
+            const uint32_t ln = __ffs(m) - 1;
+            __syncwarp();
+            if (l == 0) S.mask[L] = m & (m - 1);
+            descend(P, S, L, ln);
+            ++L;
+            open_level(P, S, L);
+        }
     }
 }
 
-template <bool WRITE>
+template <bool WRITE, int KIND>
 __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
     wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -792,15 +810,15 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
                 const uint32_t key = X.keys[k];
                 uint64_t ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
                 if (ra == rb) {
-                    run_rect<WRITE>(P, X, S, k, key, ra, ra + 1, ca, cb, sink);
+                    run_rect<WRITE, KIND>(P, X, S, k, key, ra, ra + 1, ca, cb, sink);
                     continue;
                 }
                 if (ca) {
-                    run_rect<WRITE>(P, X, S, k, key, ra, ra + 1, ca, d2, sink);
+                    run_rect<WRITE, KIND>(P, X, S, k, key, ra, ra + 1, ca, d2, sink);
                     ++ra;
                 }
-                if (ra < rb) run_rect<WRITE>(P, X, S, k, key, ra, rb, 0, d2, sink);
-                if (cb) run_rect<WRITE>(P, X, S, k, key, rb, rb + 1, 0, cb, sink);
+                if (ra < rb) run_rect<WRITE, KIND>(P, X, S, k, key, ra, rb, 0, d2, sink);
+                if (cb) run_rect<WRITE, KIND>(P, X, S, k, key, rb, rb + 1, 0, cb, sink);
             }
         }
         if (lane_id() == 0) {
@@ -814,17 +832,27 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
     }
 }
 
-static size_t block_smem(const srdl_plan *P) {
-    const uint32_t NL = P->nspec[P->depth - 1] ? P->nspec[P->depth - 1] : 1;
-    return warp_bytes(P->depth, P->natoms, NL, P->nmid) * kJoinWarps;
+static uint32_t env_u32(const char *name, uint32_t dflt) {
+    const char *v = getenv(name);
+    return v && *v ? (uint32_t)strtoul(v, nullptr, 10) : dflt;
 }
 
-template <bool WRITE>
-static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
-    const size_t bytes = block_smem(P);
+static int plan_kind(const srdl_plan *P) {
+    // SRDL_WCOJ_GENERAL=1 routes every plan through the general instance
+    // (tests cover both; also an A/B knob for the specialisation)
+    if (env_u32("SRDL_WCOJ_GENERAL", 0)) return kGeneral;
+    if (P->depth <= 2) return kShallow;
+    if (P->depth == 3 && P->nmid == 0) return kDepth3;
+    return kGeneral;
+}
+
+template <bool WRITE, int KIND>
+static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+    const uint32_t NL = P->nspec[P->depth - 1] ? P->nspec[P->depth - 1] : 1;
+    const size_t bytes = warp_bytes(P->depth, P->natoms, NL, P->nmid) * kJoinWarps;
     static bool raised = false;
     if (!raised) {  // allow up to the full 227 KB of dynamic shared memory
-        SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<WRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<WRITE, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024));
         raised = true;
     }
@@ -833,12 +861,27 @@ static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
     // the register budget decide how many fit per SM); slices are fetched
     // dynamically, so more blocks would only queue
     int per_sm = 0;
-    SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<WRITE>, kJoinWarps * 32, bytes));
+    SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<WRITE, KIND>, kJoinWarps * 32,
+                                                            bytes));
     if (per_sm < 1) per_sm = 1;
     const unsigned blocks = (unsigned)(per_sm * sm_count());
     srdl_exec x = *X;
     x.nwarps = blocks * kJoinWarps;
-    wcoj_kernel<WRITE><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, x);
+    wcoj_kernel<WRITE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, x);
+}
+
+template <bool WRITE>
+static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+    switch (plan_kind(P)) {
+        case kShallow:
+            launch_kind<WRITE, kShallow>(P, X, s);
+            break;
+        case kDepth3:
+            launch_kind<WRITE, kDepth3>(P, X, s);
+            break;
+        default:
+            launch_kind<WRITE, kGeneral>(P, X, s);
+    }
 }
 
 static void check_plan(const srdl_plan *P, const srdl_exec *X) {

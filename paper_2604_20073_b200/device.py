@@ -248,7 +248,9 @@ def col_ptrs(rows: torch.Tensor, order=None):
     order = range(arity) if order is None else order
     base = rows.data_ptr()
     stride = rows.stride(0) * 4
-    if rows.shape[1] and rows.stride(1) != 1:
+    # a single-row set may carry any stride on the row axis (e.g. a transposed
+    # (1, arity) tensor); column c still starts at base + c * stride(0)
+    if rows.shape[1] > 1 and rows.stride(1) != 1:
         raise InternalError("row set columns must be contiguous")
     ptrs = (C.c_void_p * MAX_COLS)()
     for k, c in enumerate(order):

@@ -404,6 +404,11 @@ class PlanExecution:
     def histogram(self):
         self.prep = prepare(self.plan, self.store, self.interner)
         self.partition = build_partition(self.plan, self.store, self.p, self.prep, dist=self.dist)
+        if self.plan.depth and self.prep.ok:
+            # encode now, on the calling (main) stream: the descriptor builds
+            # and caches per-index device data (dense column-0 offsets) that
+            # the count kernels of other plans, on other streams, read too
+            self.prep.descriptor()
         return self.partition
 
     def count(self) -> CountResult:

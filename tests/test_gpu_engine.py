@@ -29,8 +29,11 @@ def run(source, facts, **kw):
     return run_program(parse(source), facts, **kw)
 
 
-@pytest.mark.parametrize("schedule", ["seq", "stream"])
-def test_golden_fixpoints(golden, schedule):
+@pytest.mark.parametrize("schedule,general", [("seq", "0"), ("stream", "0"), ("stream", "1")])
+def test_golden_fixpoints(golden, schedule, general, monkeypatch):
+    # general=1: every plan through the general kernel instance instead of
+    # the depth-specialised ones (csrc/wcoj.cu plan_kind)
+    monkeypatch.setenv("SRDL_WCOJ_GENERAL", general)
     records = golden("fixpoints.json.gz")
     for rec in records:
         src = rec.get("source") or CORPUS[rec["program"]]
@@ -189,3 +192,45 @@ def test_dense_offsets_match_histogram():
     off = dev.dense_offsets(h.keys, h.prefix, 6000).cpu().numpy().astype(np.int64)
     want = np.searchsorted(col, np.arange(6001), side="left")
     assert np.array_equal(off, want)
+
+
+HASH_PROGRAM = """
+.decl Base(a:symbol, b:symbol)
+.decl E(a:symbol, b:symbol)
+.decl R(a:symbol, b:symbol)
+.decl K(a:symbol, b:symbol, c:symbol)
+.decl Tri(a:symbol, b:symbol, c:symbol)
+.decl Open(a:symbol, b:symbol, c:symbol)
+R(x, z) :- Base(x, z).
+R(x, z) :- R(x, y), E(y, z).
+K(x, y, z) :- R(x, y), E(y, z), R(x, z).
+Tri(x, y, z) :- E(x, y), E(y, z), E(z, x).
+Open(x, y, z) :- E(x, y), E(y, z), R(x, z), !E(x, z).
+"""
+
+
+@pytest.mark.parametrize("general", ["0", "1"])
+@pytest.mark.parametrize("threshold", [0, 100000])
+def test_root_invariant_leaf_sources_vs_oracle(monkeypatch, general, threshold):
+    """Leaf sources fixed by the root (R(x, z), E(z, x), the negated E(x, z))
+    next to per-parent ones, with R flushed every iteration (threshold 0) or
+    kept with a head segment; depth-specialised and general kernel."""
+    from paper_2604_20073_b200 import Engine
+
+    monkeypatch.setenv("SRDL_WCOJ_GENERAL", general)
+    rng = np.random.default_rng(12)
+    n = 400
+    a = rng.zipf(1.5, 5000) % n
+    b = rng.integers(0, n, 5000)
+    e = np.unique(np.stack([a, b], 1), axis=0)
+    e = e[e[:, 0] != e[:, 1]]
+    base = e[np.isin(e[:, 0], np.arange(0, n, 13))]
+    facts = {"E": e, "Base": base}
+    engine = Engine(parse(HASH_PROGRAM), schedule="stream", head_threshold=threshold)
+    for rel, rows in facts.items():
+        engine.load_columns(rel, rows.T.copy())
+    engine.solve()
+    want, _ = _oracle_ids(HASH_PROGRAM, facts, n)
+    for rel in ("R", "K", "Tri", "Open"):
+        got = engine.relation_columns(rel).cpu().numpy().astype(np.int64).T
+        assert np.array_equal(got, want[rel]), rel

@@ -70,3 +70,19 @@ def test_engine_fails_loudly_without_device():
 
     with pytest.raises(DeviceUnavailable):
         Engine(parse(".decl R(a:symbol)\n"))
+
+
+def test_col_ptrs_single_row_any_stride():
+    """A one-row set produced by a transpose (strides (1, arity)) is a valid
+    row set: column c starts c words after the first (regression: the
+    distributed all-gather of a single staged tuple)."""
+    import torch
+
+    t = torch.arange(2, dtype=torch.int32).view(1, 2).t().contiguous()  # (2, 1), strides (1, 2)
+    ptrs = dev.col_ptrs(t)
+    assert ptrs[1] - ptrs[0] == 4
+    wide = torch.zeros((3, 5), dtype=torch.int32)
+    ptrs = dev.col_ptrs(wide)
+    assert ptrs[2] - ptrs[0] == 2 * 5 * 4
+    with pytest.raises(Exception):
+        dev.col_ptrs(torch.zeros((5, 3), dtype=torch.int32).t())

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="triangle")
     ap.add_argument("--statements", type=int, default=1_000_000)
+    ap.add_argument("--methods", type=int, default=6_900_000, help="doop: methods (~14.5 facts each)")
     ap.add_argument("--schedule", default="stream")
     ap.add_argument("--kernels", action="store_true", help="CUPTI per-kernel totals of the last run")
     args = ap.parse_args()
@@ -33,7 +34,8 @@ def main():
     else:
         gen = {"sg": lambda: suites.sg_layered(),
                "tc": lambda: suites.tc_random(),
-               "andersen": lambda: suites.andersen_modular(args.statements, seed=1)}[args.workload]
+               "andersen": lambda: suites.andersen_modular(args.statements, seed=1),
+               "doop": lambda: suites.doop_modular(args.methods, seed=1)}[args.workload]
         facts = {k: torch.from_numpy(v).cuda() for k, v in gen().items()}
         program, out = suites.BASELINE_PROGRAMS[args.workload]
     for rep in range(2):
