@@ -32,6 +32,20 @@
 
 #include "common.cuh"
 
+// Code-size knobs (the kernel is latency-bound and its hot loops must stay
+// in the instruction cache): SRDL_LOOP keeps runtime-bounded loops rolled,
+// SRDL_SEARCH is the inlining policy of the binary-search helpers.
+#ifndef SRDL_UNROLL_LOOPS
+#define SRDL_LOOP _Pragma("unroll 1")
+#else
+#define SRDL_LOOP
+#endif
+#ifdef SRDL_NOINLINE_SEARCH
+#define SRDL_SEARCH __device__ __noinline__
+#else
+#define SRDL_SEARCH __device__ __forceinline__
+#endif
+
 namespace srdl {
 
 constexpr int kJoinWarps = 4;
@@ -43,7 +57,10 @@ constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge
 // Launch-time specialisation derived from the plan (not part of the C ABI):
 // the kernel is instantiated per plan class so each instance carries only
 // the code paths its plans can reach (smaller code, fewer i-cache misses).
-enum Kind : int { kShallow = 0, kDepth3 = 1, kGeneral = 2 };
+// kShallow: depth <= 2; kDepth3: depth 3, level 1 feeds leaf batches;
+// kDepth4Mid: depth 4 with a mid batch, level 1 feeds mid batches; kGeneral:
+// anything (DFS over the middle levels).
+enum Kind : int { kShallow = 0, kDepth3 = 1, kGeneral = 2, kDepth4Mid = 3 };
 
 
 struct Rng {
@@ -131,7 +148,7 @@ __device__ __forceinline__ View make_view(unsigned char *base, uint32_t D, uint3
     return v;
 }
 
-__device__ __forceinline__ uint32_t lbound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
+SRDL_SEARCH uint32_t lbound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
                                            uint32_t v) {
     while (lo < hi) {
         uint32_t mid = lo + ((hi - lo) >> 1);
@@ -143,7 +160,7 @@ __device__ __forceinline__ uint32_t lbound(const uint32_t *__restrict__ col, uin
     return lo;
 }
 
-__device__ __forceinline__ uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
+SRDL_SEARCH uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint32_t hi,
                                            uint32_t v) {
     while (lo < hi) {
         uint32_t mid = lo + ((hi - lo) >> 1);
@@ -157,7 +174,7 @@ __device__ __forceinline__ uint32_t ubound(const uint32_t *__restrict__ col, uin
 
 // Column-0 lookup through the index histogram: binary search over the K
 // distinct keys (a few MB, L2-resident) instead of the n rows.
-__device__ __forceinline__ bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
+SRDL_SEARCH bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
     uint32_t lo = 0, hi = A.hk;
     while (lo < hi) {
         uint32_t mid = (lo + hi) >> 1;
@@ -177,7 +194,7 @@ __device__ __forceinline__ bool hist_range(const srdl_atom &A, uint32_t v, Rng &
 
 // Narrow r (rows of segment s of atom A) to rows whose level-L columns all
 // equal v. Returns the new length (0 = no match).
-__device__ __forceinline__ void col0_range(const srdl_atom &A, uint32_t v, Rng &r) {
+SRDL_SEARCH void col0_range(const srdl_atom &A, uint32_t v, Rng &r) {
     if (A.doff) {  // dense CSR offsets: two loads
         if (v < A.dn) {
             r.lo = __ldg(A.doff + v);
@@ -190,7 +207,7 @@ __device__ __forceinline__ void col0_range(const srdl_atom &A, uint32_t v, Rng &
     }
 }
 
-__device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
+SRDL_SEARCH uint32_t narrow(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
     int c0 = A.lvl_col[L];
     const int nc = A.lvl_ncol[L];
     if (c0 == 0 && (A.hkeys || A.doff) && s == 0) {  // full segment, first column
@@ -199,6 +216,7 @@ __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uin
         c0 = 1;
     }
     uint32_t lo = r.lo, hi = r.hi;
+    SRDL_LOOP
     for (int c = c0; c < A.lvl_col[L] + nc && lo < hi; ++c) {
         const uint32_t *col = A.seg[s].cols[c];
         uint32_t a = lbound(col, lo, hi, v);
@@ -211,7 +229,7 @@ __device__ __forceinline__ uint32_t narrow(const srdl_atom &A, int s, int L, uin
     return hi - lo;
 }
 
-__device__ __forceinline__ uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
+SRDL_SEARCH uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, Rng &r) {
     if (A.lvl_col[L] == 0 && (A.hkeys || A.doff) && s == 0) {
         col0_range(A, v, r);
         return r.hi - r.lo;
@@ -233,6 +251,7 @@ struct Sink {
         const uint32_t m = __ballot_sync(kFull, alive);
         if (WRITE && alive) {
             const uint64_t pos = base + n + __popc(m & ((1u << lane_id()) - 1u));
+            SRDL_LOOP
             for (uint32_t h = 0; h < P.head_arity; ++h) {
                 const int lvl = P.head_level[h];
                 uint32_t val;
@@ -246,7 +265,9 @@ struct Sink {
                     val = S.V(leaf - 2, S.gp[parent]);
                 else
                     val = S.bind[lvl];
-                X.out[h][pos] = val;
+                // streaming store (evict-first): the output is written once and
+                // must not push the L2-resident input indexes out of L2
+                __stcs(X.out[h] + pos, val);
             }
             if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
         }
@@ -334,6 +355,7 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &
     const uint32_t nls = P.nspec[leaf];
     const uint32_t l = lane_id();
     const uint64_t total = warp_prefix(len, S.leaf_pref);
+    SRDL_LOOP
     for (uint64_t base = 0; base < total; base += 32) {
         const uint64_t f = base + l;
         bool alive = f < total;
@@ -362,10 +384,12 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &
                 Rng t = r0;
                 alive = narrow_first(D, 0, leaf, v, t) == 0;  // already produced by segment 0
             }
+            SRDL_LOOP
             for (uint32_t jj = 0; jj < nls && alive; ++jj) {
                 const srdl_atom &A = P.atom[P.spec[leaf][jj]];
                 if (jj == j && A.lvl_ncol[leaf] == 1) continue;
                 uint32_t tot = 0;
+                SRDL_LOOP
                 for (uint32_t q = 0; q < A.nseg; ++q) {
                     Rng t = S.LF(p, jj, q);
                     if (t.lo < t.hi) tot += narrow(A, q, leaf, v, t);
@@ -397,10 +421,12 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S
     bool heavy = false;
     if ((parents >> l) & 1u) {
         uint32_t best = 0xffffffffu, bj = 0, worst = 0;
+        SRDL_LOOP
         for (uint32_t j = 0; j < nls; ++j) {
             const srdl_atom &A = P.atom[P.spec[leaf][j]];
             if (A.negated) continue;
             uint32_t t = 0;
+            SRDL_LOOP
             for (uint32_t s = 0; s < A.nseg; ++s) t += S.LF(l, j, s).hi - S.LF(l, j, s).lo;
             if (t < best) {
                 best = t;
@@ -450,12 +476,14 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
     uint64_t len = 0;
     if ((gps >> l) & 1u) {
         uint32_t best = 0xffffffffu, bj = 0;
+        SRDL_LOOP
         for (uint32_t j = 0; j < P.nspec[Lm]; ++j) {
             const uint32_t a = P.spec[Lm][j];
             const srdl_atom &A = P.atom[a];
             if (A.negated) continue;
             const uint32_t slot = P.mid_slot[a];
             uint32_t t = 0;
+            SRDL_LOOP
             for (uint32_t s = 0; s < A.nseg; ++s) t += S.MD(l, slot, s).hi - S.MD(l, slot, s).lo;
             if (t < best) {
                 best = t;
@@ -468,6 +496,7 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
     const uint64_t total = warp_prefix(len, S.mid_pref);
     if (l == 0) *S.gp_active = 1u;
     __syncwarp();
+    SRDL_LOOP
     for (uint64_t base = 0; base < total; base += 32) {
         const uint64_t f = base + l;
         bool alive = f < total;
@@ -497,11 +526,13 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
                 Rng t = r0;
                 alive = narrow_first(D, 0, Lm, v, t) == 0;
             }
+            SRDL_LOOP
             for (uint32_t j = 0; j < P.nspec[Lm] && alive; ++j) {
                 const uint32_t b = P.spec[Lm][j];
                 const srdl_atom &A = P.atom[b];
                 const uint32_t slot = P.mid_slot[b], ls = P.leaf_slot[b];
                 uint32_t tot = 0;
+                SRDL_LOOP
                 for (uint32_t q = 0; q < A.nseg; ++q) {
                     Rng t = S.MD(g, slot, q);
                     if (t.lo < t.hi) tot += narrow(A, q, Lm, v, t);
@@ -511,9 +542,11 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
                 if (A.negated ? (A.check_level == Lm && tot != 0) : tot == 0) alive = false;
             }
             if (alive) {
+                SRDL_LOOP
                 for (uint32_t j = 0; j < P.nspec[leaf]; ++j) {
                     const uint32_t b = P.spec[leaf][j];
                     if (P.atom[b].lvl_ncol[Lm]) continue;
+                    SRDL_LOOP
                     for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.LF(l, j, q) = S.MD(g, P.mid_slot[b], q);
                 }
                 S.gp[l] = (uint8_t)g;
@@ -533,11 +566,13 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
 __device__ __forceinline__ void open_level(const srdl_plan &P, const View &S, int L) {
     if (lane_id() == 0) {
         uint32_t best = 0xffffffffu, ba = 0;
+        SRDL_LOOP
         for (uint32_t j = 0; j < P.nspec[L]; ++j) {
             const uint32_t a = P.spec[L][j];
             const srdl_atom &A = P.atom[a];
             if (A.negated) continue;
             uint32_t t = 0;
+            SRDL_LOOP
             for (uint32_t s = 0; s < A.nseg; ++s) t += S.R(L, a, s).hi - S.R(L, a, s).lo;
             if (t < best) {
                 best = t;
@@ -581,8 +616,9 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
         if (t.lo < t.hi) alive = narrow_first(D, 0, L, v, t) == 0;
     }
     const int leaf = (int)P.depth - 1;
-    const bool parents_level = L == leaf - 1;
-    const bool gp_level = KIND == kGeneral && P.nmid && L == leaf - 2;
+    const bool parents_level = KIND != kDepth4Mid && L == leaf - 1;
+    const bool gp_level = (KIND == kGeneral || KIND == kDepth4Mid) && P.nmid && L == leaf - 2;
+    SRDL_LOOP
     for (uint32_t j = 0; j < P.nspec[L] && alive; ++j) {
         const uint32_t b = P.spec[L][j];
         const srdl_atom &A = P.atom[b];
@@ -590,6 +626,7 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
         const bool keep = slot != SRDL_NO_ATOM;
         if (b == a && A.lvl_ncol[L] == 1 && !keep) continue;
         uint32_t tot = 0;
+        SRDL_LOOP
         for (uint32_t q = 0; q < A.nseg; ++q) {
             Rng t = S.R(L, b, q);
             if (t.lo < t.hi) tot += narrow(A, q, L, v, t);
@@ -605,17 +642,21 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
     }
     if (parents_level && alive) {
         // leaf sources not constrained at this level keep their ranges
+        SRDL_LOOP
         for (uint32_t j = 0; j < P.nspec[leaf]; ++j) {
             const uint32_t b = P.spec[leaf][j];
             if (P.atom[b].lvl_ncol[L]) continue;
+            SRDL_LOOP
             for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.LF(l, j, q) = S.R(L, b, q);
         }
     }
     if (gp_level && alive) {
         // deep sources not constrained at this level keep their ranges
+        SRDL_LOOP
         for (uint32_t b = 0; b < P.natoms; ++b) {
             const uint32_t slot = P.mid_slot[b];
             if (slot == SRDL_NO_ATOM || P.atom[b].lvl_ncol[L]) continue;
+            SRDL_LOOP
             for (uint32_t q = 0; q < P.atom[b].nseg; ++q) S.MD(l, slot, q) = S.R(L, b, q);
         }
     }
@@ -628,7 +669,7 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
     }
     __syncwarp();
     if (parents_level && m) leaf_batch<WRITE>(P, X, S, m, sink);
-    if constexpr (KIND == kGeneral) {
+    if constexpr (KIND == kGeneral || KIND == kDepth4Mid) {
         if (gp_level && m) mid_batch<WRITE>(P, X, S, m, sink);
     }
     return true;
@@ -639,6 +680,7 @@ __device__ __forceinline__ void descend(const srdl_plan &P, const View &S, int L
     const uint32_t l = lane_id();
     const uint32_t v = S.V(L, ln);
     if (l == 0) S.bind[L] = v;
+    SRDL_LOOP
     for (uint32_t t = l; t < P.natoms * SRDL_MAX_SEGS; t += 32) {
         const uint32_t a = t / SRDL_MAX_SEGS, s = t % SRDL_MAX_SEGS;
         Rng r = S.R(L, a, s);
@@ -698,6 +740,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
         lo = lo + (uint32_t)f;
     }
     if (has0 && A.lvl_ncol[0] > 1 && lo < hi) {
+        SRDL_LOOP
         for (int c = A.lvl_col[0] + 1; c < A.lvl_col[0] + A.lvl_ncol[0] && lo < hi; ++c) {
             const uint32_t *col = A.seg[s].cols[c];
             uint32_t x = lbound(col, lo, hi, key);
@@ -722,6 +765,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
             sink.emit(P, X, S, l == 0, 0, key, 0);
             return;
         }
+        SRDL_LOOP
         for (uint32_t t = l; t < P.nspec[1] * SRDL_MAX_SEGS; t += 32) {
             const uint32_t j = t / SRDL_MAX_SEGS, q = t % SRDL_MAX_SEGS;
             S.LF(0, j, q) = S.R(1, P.spec[1][j], q);
@@ -730,8 +774,9 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
         leaf_batch<WRITE>(P, X, S, 1u, sink);
         return;
     }
-    if constexpr (KIND == kDepth3) {
-        // level 1 is the parents level: chunks of it feed leaf batches
+    if constexpr (KIND == kDepth3 || KIND == kDepth4Mid) {
+        // level 1 is the parents level (depth 3) or the grandparents level
+        // of a mid batch (depth 4): its chunks feed the flattened levels
         __syncwarp();
         open_level(P, S, 1);
         while (load_chunk<WRITE, KIND>(P, X, S, 1, sink)) {
@@ -799,6 +844,7 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
                 else
                     hi = mid;
             }
+            SRDL_LOOP
             for (uint64_t k = lo; k < K; ++k) {
                 const uint64_t start = k ? X.prefix[k - 1] : 0;
                 if (start >= be) break;
@@ -843,6 +889,7 @@ static int plan_kind(const srdl_plan *P) {
     if (env_u32("SRDL_WCOJ_GENERAL", 0)) return kGeneral;
     if (P->depth <= 2) return kShallow;
     if (P->depth == 3 && P->nmid == 0) return kDepth3;
+    if (P->depth == 4 && P->nmid) return kDepth4Mid;
     return kGeneral;
 }
 
@@ -878,6 +925,9 @@ static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
             break;
         case kDepth3:
             launch_kind<WRITE, kDepth3>(P, X, s);
+            break;
+        case kDepth4Mid:
+            launch_kind<WRITE, kDepth4Mid>(P, X, s);
             break;
         default:
             launch_kind<WRITE, kGeneral>(P, X, s);

@@ -171,8 +171,10 @@ _SIGNATURES = {
 }
 
 
-def load_library(path: str = LIB_PATH):
-    """Open libsrdl.so and declare its C signatures (no CUDA needed)."""
+def load_library(path: str | None = None):
+    """Open libsrdl.so and declare its C signatures (no CUDA needed).
+    SRDL_LIBRARY names an alternative in-tree build (A/B experiments)."""
+    path = path or os.environ.get("SRDL_LIBRARY") or LIB_PATH
     if not os.path.exists(path):
         raise DeviceUnavailable(
             f"{path} is missing: build it with `python -m paper_2604_20073_b200.build` "
