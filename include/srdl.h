@@ -174,7 +174,7 @@ typedef struct {
     const uint32_t *outer_lo;  /* K first outer row of each key, or NULL       */
     const uint32_t *inner_lo;  /* K first inner row of each key, or NULL       */
     uint64_t nkeys;
-    uint32_t nwarps;         /* warps launched                                */
+    uint32_t nwarps;         /* slicing width (>= 4 x nwarps slices); same for count and materialize */
     uint32_t nslices;        /* capacity of the slice arrays                  */
     uint64_t min_units;      /* slices used = clamp(ceil(T / min_units), 1, nslices) */
     uint32_t *ticket;        /* device counter, zero before each launch       */

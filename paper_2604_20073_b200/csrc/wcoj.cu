@@ -49,7 +49,10 @@
 namespace srdl {
 
 constexpr int kJoinWarps = 4;
-constexpr int kMinBlocks = 8;  // register budget: 64K / (8 * 128) = 64 registers per thread
+#ifndef SRDL_MIN_BLOCKS
+#define SRDL_MIN_BLOCKS 8
+#endif
+constexpr int kMinBlocks = SRDL_MIN_BLOCKS;  // register budget: 64K / (8 * 128) = 64 registers per thread
 constexpr uint32_t kFull = 0xffffffffu;
 constexpr uint32_t kMergeMin = 64;    // shortest list length for merge-path leaves
 constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge-path
@@ -911,10 +914,13 @@ static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) 
     SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<WRITE, KIND>, kJoinWarps * 32,
                                                             bytes));
     if (per_sm < 1) per_sm = 1;
+    // The slice geometry (X->nwarps, nslices, min_units) comes from the
+    // caller and is identical for the count and the materialize launch; the
+    // grid is only how many warps fetch those slices, and may differ between
+    // the two instances (their occupancy can differ), so it must not feed
+    // into the slicing.
     const unsigned blocks = (unsigned)(per_sm * sm_count());
-    srdl_exec x = *X;
-    x.nwarps = blocks * kJoinWarps;
-    wcoj_kernel<WRITE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, x);
+    wcoj_kernel<WRITE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, *X);
 }
 
 template <bool WRITE>

@@ -61,6 +61,22 @@ def main():
                     rows[name] = (n + 1, t + ev.device_time_total / 1e3)
             top = sorted(rows.items(), key=lambda kv: -kv[1][1])[:14]
             print(json.dumps({"kernels_ms": {k: [n, round(t, 2)] for k, (n, t) in top}}), flush=True)
+            # device busy time = union of kernel intervals (streams overlap)
+            iv = sorted((ev.time_range.start, ev.time_range.end) for ev in prof.events()
+                        if ev.device_type == torch.autograd.DeviceType.CUDA)
+            busy, cur_s, cur_e = 0.0, None, None
+            for a, b in iv:
+                if cur_e is None or a > cur_e:
+                    if cur_e is not None:
+                        busy += cur_e - cur_s
+                    cur_s, cur_e = a, b
+                else:
+                    cur_e = max(cur_e, b)
+            if cur_e is not None:
+                busy += cur_e - cur_s
+            span = (iv[-1][1] - iv[0][0]) if iv else 0
+            print(json.dumps({"device_busy_ms": round(busy / 1e3, 2), "device_span_ms": round(span / 1e3, 2),
+                              "kernels": len(iv)}), flush=True)
         totals = {k: round(v / 1e3, 2) for k, v in sorted(stats.phase_totals().items(), key=lambda x: -x[1])}
         print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "out": summ.relations[out],
                           "iterations": [s.iterations for s in summ.strata],
