@@ -56,7 +56,9 @@ uint64_t srdl_launch_count(void);
  * (storage.py:304). Sorts n rows of `arity` columns lexicographically and
  * removes duplicates. `bits` = significant bits per id (ceil(log2(#symbols)),
  * at most 32): columns are radix-sorted on packed keys of bits*arity bits.
- * out: `arity` arrays with capacity n. *n_out = distinct rows (host). */
+ * out: `arity` arrays with capacity n. *n_out = distinct rows (host).
+ * n_out == NULL: the caller guarantees the rows are distinct (a re-sort of a
+ * delta under another column order); no host round trip, n rows written. */
 int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
                     uint32_t *const *out, uint64_t *n_out, void *stream);
 
@@ -96,6 +98,17 @@ int srdl_histogram(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *de
 int srdl_histogram_merge(const uint32_t *ka, const uint32_t *da, uint64_t na, const uint32_t *kb,
                          const uint32_t *db, uint64_t nb, uint32_t *keys, uint32_t *degrees,
                          uint64_t *prefix, uint64_t *k_out, void *stream);
+
+/* Histogram of a sorted delta column AND its union with an existing
+ * histogram (fkeys/fdeg, nf keys; nf may be 0), with one host readback
+ * (reference: Histogram.over_column + Histogram.updated, storage.py:48-76;
+ * replaces srdl_histogram + srdl_histogram_merge on the per-iteration
+ * delta path). Delta outputs hold n entries, union outputs nf + n; the
+ * first *kd_out / *ku_out are the histograms (prefix entries past them
+ * repeat the total). */
+int srdl_histogram_union(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                         uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix, uint64_t *kd_out,
+                         uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *ku_out, void *stream);
 
 /* Dense column-0 offsets from a histogram (keys[K], inclusive prefix[K]):
  * off[v] = number of rows whose column 0 is < v, for v in [0, n_ids];

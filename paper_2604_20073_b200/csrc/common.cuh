@@ -167,5 +167,6 @@ void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t 
 void inclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, cudaStream_t s);
 // stable radix sort of keys (and optional 32-bit values) on the low `bits`
 // bits; results land back in keys/vals.
-void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s);
+void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s,
+                const int *unsorted = nullptr);
 }  // namespace srdl

@@ -233,6 +233,67 @@ __global__ void rmat_kernel(uint32_t scale, uint64_t m, float a, float b, float 
     }
 }
 
+// ---- device-sized variants (lengths read from device memory): the delta
+// histogram and its union with the full histogram run back to back with a
+// single host readback at the end (srdl_histogram_union)
+
+// rank_merge_hist with |B| = *nb_dev; t runs over the capacity na + nb_cap
+__global__ void rank_merge_hist_dev(const uint32_t *__restrict__ ka, const uint32_t *__restrict__ da,
+                                    uint64_t na, const uint32_t *__restrict__ kb,
+                                    const uint32_t *__restrict__ db, const uint32_t *__restrict__ nb_dev,
+                                    uint64_t cap, uint32_t *__restrict__ mk, uint32_t *__restrict__ md) {
+    const uint64_t nb = *nb_dev;
+    const uint64_t n = na + nb;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n && t < cap;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        if (t < na) {
+            const uint32_t k = ka[t];
+            uint64_t lo = 0, hi = nb;
+            while (lo < hi) {
+                const uint64_t m = (lo + hi) >> 1;
+                if (kb[m] < k) lo = m + 1; else hi = m;
+            }
+            mk[t + lo] = k;
+            md[t + lo] = da[t];
+        } else {
+            const uint64_t j = t - na;
+            const uint32_t k = kb[j];
+            uint64_t lo = 0, hi = na;
+            while (lo < hi) {
+                const uint64_t m = (lo + hi) >> 1;
+                if (ka[m] <= k) lo = m + 1; else hi = m;
+            }
+            mk[j + lo] = k;
+            md[j + lo] = db[j];
+        }
+    }
+}
+
+// run flags over the first na + *nb_dev entries, zero up to the capacity
+__global__ void run_flags_dev(const uint32_t *__restrict__ col, uint64_t na, const uint32_t *__restrict__ nb_dev,
+                              uint64_t cap, uint32_t *__restrict__ f) {
+    const uint64_t n = na + *nb_dev;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        f[i] = i < n && ((i == 0) || col[i] != col[i - 1]);
+}
+
+__global__ void combine_pairs_dev(const uint32_t *__restrict__ mk, const uint32_t *__restrict__ md,
+                                  const uint32_t *__restrict__ f, const uint32_t *__restrict__ pos,
+                                  uint64_t na, const uint32_t *__restrict__ nb_dev, uint32_t *__restrict__ keys,
+                                  uint32_t *__restrict__ deg, uint64_t *__restrict__ deg64) {
+    const uint64_t n = na + *nb_dev;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (!f[i]) continue;
+        uint32_t d = md[i];
+        if (i + 1 < n && mk[i + 1] == mk[i]) d += md[i + 1];
+        keys[pos[i]] = mk[i];
+        deg[pos[i]] = d;
+        deg64[pos[i]] = d;
+    }
+}
+
 static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *degrees,
                                uint64_t *prefix, cudaStream_t s) {
     if (n == 0) return 0;
@@ -313,6 +374,53 @@ int srdl_histogram_merge(const uint32_t *ka, const uint32_t *da, uint64_t na, co
         SRDL_CUDA(cudaStreamSynchronize(s));
         inclusive_scan_u64(deg64.as<uint64_t>(), prefix, K, s);
         *k_out = K;
+    });
+}
+
+int srdl_histogram_union(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                         uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix, uint64_t *kd_out,
+                         uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *ku_out, void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        *kd_out = 0;
+        *ku_out = 0;
+        if (n == 0) return;
+        SRDL_REQUIRE(n + nf < (1ull << 32), "histogram_union: %llu keys exceed 2^32",
+                     (unsigned long long)(n + nf));
+        const uint64_t cap = n + nf;
+        const unsigned g = stride_grid(n), gu = stride_grid(cap);
+        Scratch f(cap * sizeof(uint32_t), s), pos(cap * sizeof(uint32_t), s), starts(n * sizeof(uint32_t), s);
+        Scratch k(sizeof(uint32_t) * 4, s), deg64(cap * sizeof(uint64_t), s);
+        uint32_t *kd = k.as<uint32_t>(), *ku = kd + 2;
+        // delta histogram (keys/degrees of the sorted column), sized on device
+        run_flags<<<g, kThreads, 0, s>>>(col, n, f.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u32(f.as<uint32_t>(), pos.as<uint32_t>(), n, kd, s);
+        run_starts<<<g, kThreads, 0, s>>>(col, f.as<uint32_t>(), pos.as<uint32_t>(), n, dkeys,
+                                          starts.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        SRDL_CUDA(cudaMemsetAsync(deg64.as<uint64_t>(), 0, n * sizeof(uint64_t), s));
+        run_lengths<<<g, kThreads, 0, s>>>(starts.as<uint32_t>(), kd, n, ddeg, deg64.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        inclusive_scan_u64(deg64.as<uint64_t>(), dprefix, n, s);  // entries >= K_d repeat the total
+        // union with the existing histogram (equal keys summed)
+        Scratch mk(cap * sizeof(uint32_t), s), md(cap * sizeof(uint32_t), s);
+        rank_merge_hist_dev<<<gu, kThreads, 0, s>>>(fkeys, fdeg, nf, dkeys, ddeg, kd, cap, mk.as<uint32_t>(),
+                                                    md.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        run_flags_dev<<<gu, kThreads, 0, s>>>(mk.as<uint32_t>(), nf, kd, cap, f.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u32(f.as<uint32_t>(), pos.as<uint32_t>(), cap, ku, s);
+        SRDL_CUDA(cudaMemsetAsync(deg64.as<uint64_t>(), 0, cap * sizeof(uint64_t), s));
+        combine_pairs_dev<<<gu, kThreads, 0, s>>>(mk.as<uint32_t>(), md.as<uint32_t>(), f.as<uint32_t>(),
+                                                  pos.as<uint32_t>(), nf, kd, ukeys, udeg, deg64.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        inclusive_scan_u64(deg64.as<uint64_t>(), uprefix, cap, s);
+        uint32_t h[4] = {0, 0, 0, 0};
+        SRDL_CUDA(cudaMemcpyAsync(h, kd, sizeof(h), cudaMemcpyDeviceToHost, s));
+        SRDL_CUDA(cudaStreamSynchronize(s));
+        *kd_out = h[0];
+        *ku_out = h[2];
     });
 }
 

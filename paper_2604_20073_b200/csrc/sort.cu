@@ -24,7 +24,9 @@ __device__ __forceinline__ uint64_t tile_index(int w, int r, int l) {
 
 // Per-block digit histogram, written digit-major: counts[d * nblocks + b].
 __global__ void __launch_bounds__(kThreads)
-    radix_hist(const uint64_t *__restrict__ keys, uint64_t n, int shift, uint32_t *counts) {
+    radix_hist(const uint64_t *__restrict__ keys, uint64_t n, int shift, uint32_t *counts,
+               const int *__restrict__ unsorted) {
+    if (unsorted && *unsorted == 0) return;  // input already in order: pass skipped
     __shared__ uint32_t h[kWarps][kBins];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&h[0][0])[i] = 0;
@@ -48,7 +50,8 @@ template <bool HAS_VALS>
 __global__ void __launch_bounds__(kThreads)
     radix_scatter(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n,
                   int shift, const uint32_t *__restrict__ offsets, uint64_t *__restrict__ keys_out,
-                  uint32_t *__restrict__ vals_out) {
+                  uint32_t *__restrict__ vals_out, const int *__restrict__ unsorted) {
+    if (unsorted && *unsorted == 0) return;
     __shared__ uint32_t cnt[kWarps][kBins];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&cnt[0][0])[i] = 0;
@@ -95,7 +98,20 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s) {
+template <class T>
+__global__ void copy_if_unsorted(T *__restrict__ dst, const T *__restrict__ src, uint64_t n,
+                                 const int *__restrict__ unsorted) {
+    if (unsorted && *unsorted == 0) return;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// `unsorted` (optional device flag): when it reads 0 every pass returns at
+// once and the keys stay in place, so a caller can skip sorting already
+// ordered input without a host round trip.
+void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s,
+                const int *unsorted) {
     if (n <= 1 || bits == 0) return;
     SRDL_REQUIRE(n < (1ull << 32), "radix_sort: %llu rows exceeds the 32-bit rank space",
                  (unsigned long long)n);
@@ -108,23 +124,32 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
     uint32_t *vin = vals, *vout = vals ? valt.as<uint32_t>() : nullptr;
     for (int p = 0; p < passes; ++p) {
         int shift = p * kRadixBits;
-        radix_hist<<<(unsigned)blocks, kThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>());
+        radix_hist<<<(unsigned)blocks, kThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>(), unsorted);
         SRDL_CHECK_LAUNCH();
         exclusive_scan_u32(counts.as<uint32_t>(), counts.as<uint32_t>(), blocks * kBins, nullptr, s);
         if (vals)
             radix_scatter<true><<<(unsigned)blocks, kThreads, 0, s>>>(
-                kin, vin, n, shift, counts.as<uint32_t>(), kout, vout);
+                kin, vin, n, shift, counts.as<uint32_t>(), kout, vout, unsorted);
         else
             radix_scatter<false><<<(unsigned)blocks, kThreads, 0, s>>>(
-                kin, nullptr, n, shift, counts.as<uint32_t>(), kout, nullptr);
+                kin, nullptr, n, shift, counts.as<uint32_t>(), kout, nullptr, unsorted);
         SRDL_CHECK_LAUNCH();
         std::swap(kin, kout);
         std::swap(vin, vout);
     }
     if (kin != keys) {
-        SRDL_CUDA(cudaMemcpyAsync(keys, kin, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-        if (vals)
-            SRDL_CUDA(cudaMemcpyAsync(vals, vin, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        if (unsorted) {  // skipped passes left the keys in place
+            copy_if_unsorted<<<stride_grid(n), kThreads, 0, s>>>(keys, kin, n, unsorted);
+            SRDL_CHECK_LAUNCH();
+            if (vals) {
+                copy_if_unsorted<<<stride_grid(n), kThreads, 0, s>>>(vals, vin, n, unsorted);
+                SRDL_CHECK_LAUNCH();
+            }
+        } else {
+            SRDL_CUDA(cudaMemcpyAsync(keys, kin, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            if (vals)
+                SRDL_CUDA(cudaMemcpyAsync(vals, vin, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        }
     }
 }
 
@@ -311,9 +336,15 @@ static bool rows_sorted(const Cols &rows, uint64_t n, uint32_t arity, bool stric
 }
 
 // Sort + unique + anti-join; the heart of compute_delta.
+// Inputs up to this many rows decide "already sorted?" on the device (the
+// radix passes skip themselves) instead of with a host round trip; larger
+// inputs take the host branch, where the sorted fast path avoids the key
+// packing altogether and one round trip is noise.
+constexpr uint64_t kDeviceBranchRows = 1ull << 22;
+
 static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, uint64_t n,
                                   uint32_t bits, const Segs &S, uint32_t *const *out,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, bool want_count = true) {
     SRDL_REQUIRE(arity >= 1 && arity <= SRDL_MAX_COLS, "arity %u outside [1, %d]", arity,
                  SRDL_MAX_COLS);
     SRDL_REQUIRE(bits >= 1 && bits <= 32, "bits %u outside [1, 32]", bits);
@@ -326,7 +357,16 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
     Scratch keep(n * sizeof(uint32_t), s);
     Scratch total(sizeof(uint32_t) * 2, s);
     const uint32_t per_chunk = 64 / bits;
-    if (rows_sorted(in, n, arity, false, s)) {
+    const bool device_branch = n <= kDeviceBranchRows;
+    Scratch unsorted(sizeof(int), s);
+    const int *uns = nullptr;
+    if (device_branch) {
+        SRDL_CUDA(cudaMemsetAsync(unsorted.as<int>(), 0, sizeof(int), s));
+        check_sorted<<<stride_grid(n), kThreads, 0, s>>>(in, n, arity, 0, unsorted.as<int>());
+        SRDL_CHECK_LAUNCH();
+        uns = unsorted.as<int>();
+    }
+    if (!device_branch && rows_sorted(in, n, arity, false, s)) {
         // staged rows already in index order (e.g. WCOJ output enumerated in
         // variable order): unique + anti-join without sorting
         flag_rows<<<g, kThreads, 0, s>>>(in, n, arity, keep.as<uint32_t>());
@@ -339,7 +379,7 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
     } else if (arity <= per_chunk) {
         pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, arity}, bits, nullptr, n, keys.as<uint64_t>());
         SRDL_CHECK_LAUNCH();
-        radix_sort(keys.as<uint64_t>(), nullptr, n, arity * bits, s);
+        radix_sort(keys.as<uint64_t>(), nullptr, n, arity * bits, s, uns);
         flag_keys<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), n, keep.as<uint32_t>());
         SRDL_CHECK_LAUNCH();
         anti_join_keys(keys.as<uint64_t>(), n, S, arity, bits, keep.as<uint32_t>(), s);
@@ -361,7 +401,7 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
             pack_keys<<<g, kThreads, 0, s>>>(in, ch, bits, perm.as<uint32_t>(), n,
                                              keys.as<uint64_t>());
             SRDL_CHECK_LAUNCH();
-            radix_sort(keys.as<uint64_t>(), perm.as<uint32_t>(), n, ch.count * bits, s);
+            radix_sort(keys.as<uint64_t>(), perm.as<uint32_t>(), n, ch.count * bits, s, uns);
             end = first;
         }
         Scratch sorted(n * sizeof(uint32_t) * arity, s);
@@ -382,6 +422,7 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
                                             dst);
         SRDL_CHECK_LAUNCH();
     }
+    if (!want_count) return n;  // caller guarantees distinct rows: no round trip
     uint32_t cnt = 0;
     SRDL_CUDA(cudaMemcpyAsync(&cnt, total.as<uint32_t>(), sizeof(cnt), cudaMemcpyDeviceToHost, s));
     SRDL_CUDA(cudaStreamSynchronize(s));
@@ -399,7 +440,9 @@ int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uin
     return guarded([&] {
         Segs none{};
         none.nseg = 0;
-        *n_out = sort_unique_minus(cols, arity, n, bits, none, out, (cudaStream_t)stream);
+        const uint64_t got = sort_unique_minus(cols, arity, n, bits, none, out, (cudaStream_t)stream,
+                                               n_out != nullptr);
+        if (n_out) *n_out = got;
     });
 }
 

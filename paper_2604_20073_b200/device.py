@@ -135,6 +135,11 @@ _SIGNATURES = {
         [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
          C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
     ),
+    "srdl_histogram_union": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
+    ),
     "srdl_dense_offsets": (
         C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]
     ),
@@ -267,8 +272,9 @@ def sym_bits(nsym: int) -> int:
 # ------------------------------------------------------------- operations
 
 
-def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None) -> torch.Tensor:
-    """Distinct rows sorted lexicographically (columns taken in `order`)."""
+def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None, distinct: bool = False) -> torch.Tensor:
+    """Distinct rows sorted lexicographically (columns taken in `order`).
+    distinct=True: the rows are known to be distinct (no host round trip)."""
     arity, n = rows.shape
     order = list(range(arity)) if order is None else list(order)
     out = empty_rows(len(order), n)
@@ -277,10 +283,10 @@ def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None) -> torch.Tensor:
     got = C.c_uint64(0)
     check(
         lib().srdl_sort_dedup(col_ptrs(rows, order), len(order), n, bits, col_ptrs(out),
-                              C.byref(got), stream_handle()),
+                              None if distinct else C.byref(got), stream_handle()),
         "sort_dedup",
     )
-    return _trim(out, got.value)
+    return out if distinct else _trim(out, got.value)
 
 
 def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
@@ -367,6 +373,28 @@ def histogram_merge(ka, da, kb, db):
                                      C.byref(k), stream_handle()), "histogram_merge")
     K = k.value
     return keys[:K], deg[:K], prefix[:K]
+
+
+def histogram_union(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor):
+    """(delta histogram of the sorted column, union with (fkeys, fdeg)) as two
+    (keys, degrees, prefix) triples, one host round trip."""
+    n, nf = col.numel(), fkeys.numel()
+    d = device()
+    dk = torch.empty(n, dtype=U32, device=d)
+    dd = torch.empty(n, dtype=U32, device=d)
+    dp = torch.empty(n, dtype=U64, device=d)
+    uk = torch.empty(n + nf, dtype=U32, device=d)
+    ud = torch.empty(n + nf, dtype=U32, device=d)
+    up = torch.empty(n + nf, dtype=U64, device=d)
+    if n == 0:
+        return (dk, dd, dp), (fkeys, fdeg, None)
+    kd, ku = C.c_uint64(0), C.c_uint64(0)
+    check(lib().srdl_histogram_union(col.data_ptr(), n, fkeys.data_ptr() if nf else None,
+                                     fdeg.data_ptr() if nf else None, nf, dk.data_ptr(), dd.data_ptr(),
+                                     dp.data_ptr(), C.byref(kd), uk.data_ptr(), ud.data_ptr(), up.data_ptr(),
+                                     C.byref(ku), stream_handle()), "histogram_union")
+    a, b = kd.value, ku.value
+    return (dk[:a], dd[:a], dp[:a]), (uk[:b], ud[:b], up[:b])
 
 
 def dense_offsets(keys, prefix, n_ids: int) -> torch.Tensor:

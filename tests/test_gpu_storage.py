@@ -168,3 +168,53 @@ def test_anti_join_small_staged_vs_large_full(dev):
     staged3 = np.concatenate([staged, staged[:, :1]], axis=1)
     got3 = dev.compute_delta(to_dev(staged3, 3), [to_dev(full3, 3)], 32)  # row-compare path
     assert np.array_equal(host(got3)[:, :2], want)
+
+
+@pytest.mark.parametrize("n,nf", [(0, 50), (1, 0), (7, 0), (3000, 0), (1, 1), (5000, 20000), (300_000, 2_000)])
+def test_histogram_union_matches_two_step(dev, n, nf):
+    """srdl_histogram_union == histogram(delta) and its union with a full
+    histogram (equal keys summed), overlapping and disjoint key sets."""
+    rng = np.random.default_rng(n + 7 * nf)
+    col = np.sort(rng.zipf(1.4, size=n) % 50_000).astype(np.uint32)
+    full = np.sort(rng.integers(0, 60_000, size=nf)).astype(np.uint32)
+    fk, fd, _ = dev.histogram(torch.from_numpy(full).to(dev.device()))
+    (dk, dd, dp), (uk, ud, up) = dev.histogram_union(torch.from_numpy(col).to(dev.device()), fk, fd)
+    ck, cc = np.unique(col, return_counts=True)
+    assert np.array_equal(dk.cpu().numpy(), ck)
+    assert np.array_equal(dd.cpu().numpy(), cc)
+    assert np.array_equal(dp.cpu().numpy(), np.cumsum(cc))
+    if n:
+        both = np.concatenate([col, full])
+        bk, bc = np.unique(both, return_counts=True)
+        assert np.array_equal(uk.cpu().numpy(), bk)
+        assert np.array_equal(ud.cpu().numpy(), bc)
+        assert np.array_equal(up.cpu().numpy(), np.cumsum(bc))
+
+
+@pytest.mark.parametrize("arity,bits", [(1, 21), (2, 16), (3, 32)])
+@pytest.mark.parametrize("layout", ["random", "sorted", "sorted_dups"])
+@pytest.mark.parametrize("n", [2, 1000, 200_000, 5_000_000])
+def test_sort_paths_device_and_host_branch(dev, arity, bits, layout, n):
+    """sort_dedup / compute_delta decide 'already sorted' on the device below
+    2^22 rows (radix passes skip themselves) and on the host above; both
+    branches, every key-packing path (1 chunk, 3x32-bit multi-chunk), sorted
+    and unsorted input, and the distinct=True re-sort."""
+    rng = np.random.default_rng(n + arity)
+    hi = min(1 << bits, 1 << 20)
+    rows = rng.integers(0, hi, size=(n, arity))
+    if layout != "random":
+        rows = np.unique(rows, axis=0) if layout == "sorted" else rows[np.lexsort(rows.T[::-1])]
+    want = np.unique(rows, axis=0)
+    t = to_dev(rows.reshape(-1), arity)
+    got = dev.sort_dedup(t, bits)
+    assert np.array_equal(host(got), want)
+    full = want[::3]
+    fd = to_dev(full.reshape(-1), arity)
+    delta = dev.compute_delta(t, [fd], bits)
+    keep = ~np.isin(np.arange(len(want)), np.arange(0, len(want), 3))
+    assert np.array_equal(host(delta), want[keep])
+    if arity > 1:  # distinct rows re-sorted under the reversed column order
+        order = list(range(arity))[::-1]
+        rs = dev.sort_dedup(got, bits, order=order, distinct=True)
+        ref = want[:, order]
+        assert np.array_equal(host(rs), ref[np.lexsort(ref.T[::-1])])
