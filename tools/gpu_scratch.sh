@@ -1,7 +1,6 @@
 O=gpurun_out
-export PYTHONFAULTHANDLER=1
-timeout 1200 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
-for w in triangle sg andersen doop tc; do timeout 600 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > $O/s_$w.json 2>$O/s_$w.err; done
-for w in sg doop; do timeout 600 python tools/phase_report.py --workload $w --kernels > $O/busy3_$w.txt 2>&1; done
-timeout 600 env SRDL_LIBRARY=$PWD/paper_2604_20073_b200/libsrdl_mb5.so python bench.py --workload sg --steps 3 --warmup 3 --no-cpu-baseline > $O/s_mb5_sg.json 2>$O/s_mb5_sg.err
+timeout 900 python tools/phase_report.py --workload doop --schedule seq --rules 25 > $O/rules_doop.txt 2>&1
+timeout 600 python tools/phase_report.py --workload sg --schedule seq --rules 12 > $O/rules_sg.txt 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:wcoj_kernel -c 2 -o $O/prof_tri_v5 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_tri.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on --replay-mode application -k regex:wcoj_kernel -s 1 -c 1 -o $O/prof_tri_mat_s18 python bench.py --scale 18 --edges 4000000 --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_tri_mat.log 2>&1
 exit 0

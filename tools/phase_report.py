@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--methods", type=int, default=6_900_000, help="doop: methods (~14.5 facts each)")
     ap.add_argument("--schedule", default="stream")
     ap.add_argument("--kernels", action="store_true", help="CUPTI per-kernel totals of the last run")
+    ap.add_argument("--rules", type=int, default=0, help="print the N costliest (rule, phase) pairs")
     args = ap.parse_args()
     if args.workload == "triangle":
         raw = dev.gen_rmat(20, 16_000_000, seed=1).view(torch.int32)
@@ -78,6 +79,15 @@ def main():
             print(json.dumps({"device_busy_ms": round(busy / 1e3, 2), "device_span_ms": round(span / 1e3, 2),
                               "kernels": len(iv)}), flush=True)
         totals = {k: round(v / 1e3, 2) for k, v in sorted(stats.phase_totals().items(), key=lambda x: -x[1])}
+        if stats.enabled and args.rules:
+            per = {}
+            for r in stats.records:
+                key = f"{r['rule']}:{r['phase']}"
+                t, n = per.get(key, (0, 0))
+                per[key] = (t + r["micros"], n + r["tuples"])
+            top = sorted(per.items(), key=lambda kv: -kv[1][0])[:args.rules]
+            print(json.dumps({"top_rule_phases_ms": {k: [round(t / 1e3, 2), n] for k, (t, n) in top}}),
+                  flush=True)
         print(json.dumps({"rep": rep, "wall_s": round(wall, 3), "out": summ.relations[out],
                           "iterations": [s.iterations for s in summ.strata],
                           "phase_ms": totals}), flush=True)
