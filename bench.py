@@ -286,14 +286,15 @@ def flush_l2(torch, buf):
     buf.add_(1)  # 512 MiB write > 126 MB L2
 
 
-def load_profile_traffic(workload_name):
-    """dram bytes per launch of the dominant kernel from a committed ncu capture."""
+def load_profile_traffic(workload_name, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    capture (profiles/wcoj_traffic.json, written by tools/traffic_summary.py)."""
     path = os.path.join(ROOT, "profiles", "wcoj_traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as fh:
         d = json.load(fh)
-    return d.get(workload_name)
+    return (d.get(workload_name) or {}).get(kernel)
 
 
 # --------------------------------------------------------------------------
@@ -423,7 +424,7 @@ def bench_ours(args, rank, world, dist):
             "peak_source": src,
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
-            "traffic": load_profile_traffic(wl.name),
+            "traffic": load_profile_traffic(wl.name, name),
             "algorithmic_bytes_per_launch": algo,
             "launch_ms": round(per_launch * 1e3, 3),
             "launches_per_step": len(kern[name]) / args.steps,

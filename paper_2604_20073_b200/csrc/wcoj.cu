@@ -54,8 +54,11 @@ constexpr int kJoinWarps = 4;
 #endif
 constexpr int kMinBlocks = SRDL_MIN_BLOCKS;  // register budget: 64K / (8 * 128) = 64 registers per thread
 constexpr uint32_t kFull = 0xffffffffu;
-constexpr uint32_t kMergeMin = 64;    // shortest list length for merge-path leaves
-constexpr uint32_t kMergeRatio = 16;  // longest / shortest list ratio for merge-path
+// merge-path leaves: both lists at least c_merge_min long and within a
+// factor c_merge_ratio of each other (otherwise per-candidate binary search);
+// defaults 64 / 16, SRDL_MERGE_MIN / SRDL_MERGE_RATIO override (sweeps)
+__constant__ uint32_t c_merge_min = 64;
+__constant__ uint32_t c_merge_ratio = 16;
 
 // Launch-time specialisation derived from the plan (not part of the C ABI):
 // the kernel is instantiated per plan class so each instance carries only
@@ -245,6 +248,37 @@ SRDL_SEARCH uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, 
     return b - a;
 }
 
+// One head tuple at output row `pos` (materialize only). Inlined into every
+// emit site: an out-of-line copy (SRDL_NOINLINE_STORE) shrinks the code but
+// measured slower (triangle materialize 94 -> 111 ms).
+#ifdef SRDL_NOINLINE_STORE
+#define SRDL_STORE __device__ __noinline__
+#else
+#define SRDL_STORE __device__ __forceinline__
+#endif
+SRDL_STORE void store_tuple(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t pos,
+                            uint32_t parent, uint32_t v, int leaf) {
+    SRDL_LOOP
+    for (uint32_t h = 0; h < P.head_arity; ++h) {
+        const int lvl = P.head_level[h];
+        uint32_t val;
+        if (lvl < 0)
+            val = P.head_const[h];
+        else if (lvl == leaf)
+            val = v;
+        else if (lvl == leaf - 1)
+            val = S.V(leaf - 1, parent);
+        else if (lvl == leaf - 2 && *S.gp_active)
+            val = S.V(leaf - 2, S.gp[parent]);
+        else
+            val = S.bind[lvl];
+        // streaming store (evict-first): the output is written once and
+        // must not push the L2-resident input indexes out of L2
+        __stcs(X.out[h] + pos, val);
+    }
+    if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
+}
+
 template <bool WRITE>
 struct Sink {
     uint64_t n;       // tuples emitted so far in this slice (uniform)
@@ -252,28 +286,8 @@ struct Sink {
     __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const View &S,
                                          bool alive, uint32_t parent, uint32_t v, int leaf) {
         const uint32_t m = __ballot_sync(kFull, alive);
-        if (WRITE && alive) {
-            const uint64_t pos = base + n + __popc(m & ((1u << lane_id()) - 1u));
-            SRDL_LOOP
-            for (uint32_t h = 0; h < P.head_arity; ++h) {
-                const int lvl = P.head_level[h];
-                uint32_t val;
-                if (lvl < 0)
-                    val = P.head_const[h];
-                else if (lvl == leaf)
-                    val = v;
-                else if (lvl == leaf - 1)
-                    val = S.V(leaf - 1, parent);
-                else if (lvl == leaf - 2 && *S.gp_active)
-                    val = S.V(leaf - 2, S.gp[parent]);
-                else
-                    val = S.bind[lvl];
-                // streaming store (evict-first): the output is written once and
-                // must not push the L2-resident input indexes out of L2
-                __stcs(X.out[h] + pos, val);
-            }
-            if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
-        }
+        if (WRITE && alive)
+            store_tuple(P, X, S, base + n + __popc(m & ((1u << lane_id()) - 1u)), parent, v, leaf);
         n += __popc(m);
     }
 };
@@ -439,7 +453,7 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S
         }
         len = best;
         S.leaf_drv[l] = (uint8_t)bj;
-        if (pairable && best >= kMergeMin && worst <= best * kMergeRatio) {
+        if (pairable && best >= c_merge_min && (uint64_t)worst <= (uint64_t)best * c_merge_ratio) {
             const Rng a1 = S.LF(l, 0, 1), b1 = S.LF(l, 1, 1);
             const bool single = (P.atom[P.spec[leaf][0]].nseg < 2 || a1.lo >= a1.hi) &&
                                 (P.atom[P.spec[leaf][1]].nseg < 2 || b1.lo >= b1.hi);
@@ -923,8 +937,24 @@ static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) 
     wcoj_kernel<WRITE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, *X);
 }
 
+static void apply_tuning() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const char *a = getenv("SRDL_MERGE_MIN"), *b = getenv("SRDL_MERGE_RATIO");
+    if (a && *a) {
+        const uint32_t v = (uint32_t)strtoul(a, nullptr, 10);
+        SRDL_CUDA(cudaMemcpyToSymbol(c_merge_min, &v, sizeof(v)));
+    }
+    if (b && *b) {
+        const uint32_t v = (uint32_t)strtoul(b, nullptr, 10);
+        SRDL_CUDA(cudaMemcpyToSymbol(c_merge_ratio, &v, sizeof(v)));
+    }
+}
+
 template <bool WRITE>
 static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+    apply_tuning();
     switch (plan_kind(P)) {
         case kShallow:
             launch_kind<WRITE, kShallow>(P, X, s);

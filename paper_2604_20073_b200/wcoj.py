@@ -21,6 +21,7 @@ the kernel uses max(p, DEVICE_WARPS) slices; results do not depend on it.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -35,7 +36,7 @@ from .syntax import VAR
 
 WARPS_PER_SM = 32  # slice-array sizing; the launcher picks the resident wave itself
 SLICES_PER_WARP = 256  # slice-array capacity per launched warp (fetched dynamically)
-MIN_SLICE_UNITS = 4096  # fewer, larger slices when the root space is small
+MIN_SLICE_UNITS = int(os.environ.get("SRDL_MIN_SLICE_UNITS", 4096))  # fewer, larger slices when the root space is small
 
 # Benchmark hook: when a list, every count/materialize launch appends
 # (name, start_event, end_event) recorded on the launching stream.

@@ -1,6 +1,7 @@
 O=gpurun_out
-timeout 900 python tools/phase_report.py --workload doop --schedule seq --rules 25 > $O/rules_doop.txt 2>&1
-timeout 600 python tools/phase_report.py --workload sg --schedule seq --rules 12 > $O/rules_sg.txt 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:wcoj_kernel -c 2 -o $O/prof_tri_v5 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_tri.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on --replay-mode application -k regex:wcoj_kernel -s 1 -c 1 -o $O/prof_tri_mat_s18 python bench.py --scale 18 --edges 4000000 --steps 1 --warmup 0 --no-cpu-baseline > $O/ncu_tri_mat.log 2>&1
+for v in default istore; do
+  lib=""; [ $v != default ] && lib="SRDL_LIBRARY=$PWD/paper_2604_20073_b200/libsrdl_$v.so"
+  for w in triangle sg andersen doop; do timeout 600 env $lib python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > $O/t_${v}_$w.json 2>$O/t_${v}_$w.err; done
+done
+timeout 900 python -m pytest tests/test_gpu_engine.py -m gpu -q -x > $O/pytest_engine.log 2>&1; echo "rc=$?" >> $O/pytest_engine.log
 exit 0
