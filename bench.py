@@ -18,13 +18,18 @@ e2e      same step through the public API with pinned HOST inputs: the H2D
 roofline the dominant kernel (WCOJ count/materialize), CUDA events on its
          stream over the timed steps, algorithmic bytes / duration vs the
          measured HBM copy bandwidth (MEASURED_PEAKS.json).
-cpu_baseline / --impl reference
+cpu_baseline
          the numpy oracle restatement of the reference algorithm on a bounded
-         sample of the same workload (a subset of root keys), 1 host core.
+         sample of the same workload (a subset of root keys, or a scaled-down
+         instance for recursive workloads), 1 host core.
+--impl reference
+         the same restatement on all host cores (triangle: root keys dealt to
+         forked workers; recursive workloads: 1 core, iterations are serial).
 
-Multi-GPU (torchrun): root keys are hash-partitioned across ranks (x mod N),
-each rank evaluates its partition with no data-path collective; the timing is
-the max over ranks (NCCL all-reduce on the timings only).
+Multi-GPU (torchrun): the triangle hash-partitions its root keys across
+ranks (x mod N) with no data-path collective; recursive workloads run the
+distributed engine (per-iteration all-to-all of new tuples + all-reduce of
+delta sizes). Timing is the max over ranks.
 """
 
 from __future__ import annotations
@@ -80,9 +85,6 @@ class Workload:
         """-> {relation: (2, n) uint32 device tensor} (this rank's share)."""
         raise NotImplementedError
 
-    def algorithmic_bytes(self, inputs: dict, n_out: int) -> int:
-        raise NotImplementedError
-
 
 class TriangleRMAT(Workload):
     name = "triangle-rmat"
@@ -121,14 +123,6 @@ class TriangleRMAT(Workload):
         r = ei[:, (ei[0] % w) == self.rank].contiguous().view(torch.uint32)
         t = ei[:, (ei[1] % w) == self.rank].contiguous().view(torch.uint32)
         return {"R": r, "S": e, "T": t}
-
-    def algorithmic_bytes(self, inputs, n_out):
-        # each WCOJ launch must read the three sorted edge indexes once
-        # (2 x u32 per edge) and the root work arrays; materialize also
-        # writes 3 x u32 per derived tuple
-        edge_bytes = sum(8 * int(t.shape[1]) for t in inputs.values())
-        return edge_bytes, 12 * n_out
-
 
 class Recursive(Workload):
     """A recursive BASELINE workload: integer-column EDB from
@@ -170,9 +164,6 @@ class Recursive(Workload):
         facts = (self._sample if self.small else self._full)()
         self.config["edb_facts"] = int(sum(v.shape[1] for v in facts.values()))
         return {k: torch.from_numpy(v).to(dev.device()) for k, v in facts.items()}
-
-    def algorithmic_bytes(self, inputs, n_out):
-        return 8 * sum(int(t.shape[1]) for t in inputs.values()), 8 * n_out
 
     def cpu_sample(self):
         from oracle.gj import Symbols, fixpoint
@@ -403,19 +394,20 @@ def bench_ours(args, rank, world, dist):
             dist.all_reduce(c)
             tot_out = int(c.item())
 
-    # dominant kernel roofline
-    kern = {}
-    for name, a, b in events:
+    # dominant kernel roofline: per launch, algorithmic bytes (every input
+    # index segment read once + derived tuples written once, recorded by
+    # wcoj._timed) over the CUDA-event time on the launching stream
+    kern, kbytes = {}, {}
+    for name, a, b, nbytes in events:
         kern.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
+        kbytes[name] = kbytes.get(name, 0) + nbytes
     roofline = None
     if kern:
         name = max(kern, key=lambda k: sum(kern[k]))
         per_launch = sum(kern[name]) / len(kern[name])
-        in_bytes, out_bytes = wl.algorithmic_bytes({k: v for k, v in inputs.items() if not k.startswith("_")},
-                                                   n_out)
-        algo = in_bytes + (out_bytes if name == "wcoj_materialize" else 0)
+        algo = kbytes[name] / len(kern[name])
         peak, src = measured_peaks()
-        achieved = algo / per_launch / 1e9
+        achieved = kbytes[name] / sum(kern[name]) / 1e9
         roofline = {
             "bound": "hbm",
             "kernel": name,
@@ -425,7 +417,9 @@ def bench_ours(args, rank, world, dist):
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": load_profile_traffic(wl.name, name),
-            "algorithmic_bytes_per_launch": algo,
+            "algorithmic_bytes_per_launch": int(algo),
+            "algorithmic_bytes_model": "4 B x columns x rows of every index segment the plan reads, once; "
+                                       "+ 4 B x head arity per derived tuple (materialize)",
             "launch_ms": round(per_launch * 1e3, 3),
             "launches_per_step": len(kern[name]) / args.steps,
             "kernel_share_of_step": round(sum(kern[name]) / sum(times), 4),

@@ -43,7 +43,10 @@ MIN_SLICE_UNITS = int(os.environ.get("SRDL_MIN_SLICE_UNITS", 4096))  # fewer, la
 KERNEL_EVENTS = None
 
 
-def _timed(name, fn):
+def _timed(name, fn, algo_bytes=0):
+    """Run fn; when KERNEL_EVENTS is a list (bench.py), bracket it with CUDA
+    events on the current (launching) stream and record the launch's
+    algorithmic bytes next to them."""
     if KERNEL_EVENTS is None:
         return fn()
     a = torch.cuda.Event(enable_timing=True)
@@ -51,8 +54,14 @@ def _timed(name, fn):
     a.record()
     rc = fn()
     b.record()
-    KERNEL_EVENTS.append((name, a, b))
+    KERNEL_EVENTS.append((name, a, b, algo_bytes))
     return rc
+
+
+def input_bytes(prep) -> int:
+    """Algorithmic input bytes of one WCOJ launch: every column of every
+    index segment the plan reads, once (4 B per id)."""
+    return sum(4 * pa.arity * (hi - lo) for pa, src in zip(prep.plan.atoms, prep.segs) for _, lo, hi in src)
 
 
 def device_warps(p: int = 1) -> int:
@@ -354,7 +363,8 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
     dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x),
-                                                                      dev.stream_handle())), "wcoj_count")
+                                                                      dev.stream_handle()),
+                     input_bytes(prep) if KERNEL_EVENTS is not None else 0), "wcoj_count")
     return counts
 
 
@@ -377,8 +387,10 @@ def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep
         error = torch.zeros(1, dtype=torch.int32, device=dev.device())
     desc = prep.descriptor()
     x = _exec_desc(partition, counts, out_cols, error, bitmap)
+    out_bytes = 4 * plan.head_arity * total  # every derived tuple written once
     dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
-        C.byref(desc), C.byref(x), dev.stream_handle())), "wcoj_materialize")
+        C.byref(desc), C.byref(x), dev.stream_handle()),
+        input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize")
     if own_flag and int(error.item()):
         raise InternalError(f"plan {plan.plan_id}: materialized tuple count diverged from the count pass")
     return out_cols
