@@ -45,14 +45,28 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
-// Stable scatter: rank within the tile via warp match + per-warp counters.
+// Stable scatter: rank within the tile via warp match + per-warp counters,
+// then the tile is reordered by digit in shared memory and written out with
+// consecutive threads storing consecutive positions of each digit's run
+// (coalesced; a direct per-key store would touch one sector per key).
+template <bool HAS_VALS>
+constexpr size_t scatter_smem() {
+    return (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0) + (size_t)kWarps * kBins * 4 +
+           (size_t)kBins * 8 + 64 * 4;
+}
+
 template <bool HAS_VALS>
 __global__ void __launch_bounds__(kThreads)
     radix_scatter(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n,
                   int shift, const uint32_t *__restrict__ offsets, uint64_t *__restrict__ keys_out,
                   uint32_t *__restrict__ vals_out, const int *__restrict__ unsorted) {
     if (unsorted && *unsorted == 0) return;
-    __shared__ uint32_t cnt[kWarps][kBins];
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint64_t *skeys = (uint64_t *)sm;
+    uint32_t *svals = (uint32_t *)(sm + (size_t)kTile * 8);
+    uint32_t(*cnt)[kBins] = (uint32_t(*)[kBins])(sm + (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0));
+    int64_t *gbase = (int64_t *)((unsigned char *)cnt + (size_t)kWarps * kBins * 4);
+    uint32_t *wsum = (uint32_t *)(gbase + kBins);  // [kWarps] scan carries
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&cnt[0][0])[i] = 0;
     __syncthreads();
@@ -76,25 +90,51 @@ __global__ void __launch_bounds__(kThreads)
         rank[r] = before + __popc(peers & lt);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kBins; d += kThreads) {
-        uint32_t run = offsets[(uint64_t)d * gridDim.x + blockIdx.x];
+    // digit d (one per thread, kThreads == kBins): per-warp exclusive offsets
+    // within the digit, then a block-wide exclusive scan of the digit totals
+    static_assert(kThreads == kBins, "one thread per digit");
+    const int d = threadIdx.x;
+    uint32_t total = 0;
 #pragma unroll
-        for (int q = 0; q < kWarps; ++q) {
-            uint32_t c = cnt[q][d];
-            cnt[q][d] = run;
-            run += c;
-        }
+    for (int q = 0; q < kWarps; ++q) {
+        const uint32_t c = cnt[q][d];
+        cnt[q][d] = total;
+        total += c;
     }
+    uint32_t incl = total;  // inclusive scan of totals across the block
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (l >= o) incl += y;
+    }
+    if (l == 31) wsum[w] = incl;
+    __syncthreads();
+    uint32_t carry = 0;
+    for (int q = 0; q < w; ++q) carry += wsum[q];
+    const uint32_t local_start = carry + incl - total;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) cnt[q][d] += local_start;
+    gbase[d] = (int64_t)offsets[(uint64_t)d * gridDim.x + blockIdx.x] - (int64_t)local_start;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         uint64_t i = tile_index(w, r, l);
         if (i < n) {
-            uint32_t d = (uint32_t)((k[r] >> shift) & (kBins - 1));
-            uint32_t pos = cnt[w][d] + rank[r];
-            keys_out[pos] = k[r];
-            if (HAS_VALS) vals_out[pos] = v[r];
+            const uint32_t dd = (uint32_t)((k[r] >> shift) & (kBins - 1));
+            const uint32_t lpos = cnt[w][dd] + rank[r];
+            skeys[lpos] = k[r];
+            if (HAS_VALS) svals[lpos] = v[r];
         }
+    }
+    __syncthreads();
+    const uint64_t base = (uint64_t)blockIdx.x * kTile;
+    const uint32_t here = n - base < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
+    for (uint32_t i = threadIdx.x; i < here; i += kThreads) {
+        const uint64_t key = skeys[i];
+        const uint32_t dd = (uint32_t)((key >> shift) & (kBins - 1));
+        const uint64_t pos = (uint64_t)(gbase[dd] + (int64_t)i);
+        keys_out[pos] = key;
+        if (HAS_VALS) vals_out[pos] = svals[i];
     }
 }
 
@@ -117,6 +157,14 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
                  (unsigned long long)n);
     const uint64_t blocks = (n + kTile - 1) / kTile;
     const int passes = (int)((bits + kRadixBits - 1) / kRadixBits);
+    static bool raised = false;
+    if (!raised) {  // the reorder tile needs more than the 48 KB default
+        SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)scatter_smem<true>()));
+        SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)scatter_smem<false>()));
+        raised = true;
+    }
     Scratch kalt(n * sizeof(uint64_t), s);
     Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);
     Scratch counts(blocks * kBins * sizeof(uint32_t), s);
@@ -128,10 +176,10 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
         SRDL_CHECK_LAUNCH();
         exclusive_scan_u32(counts.as<uint32_t>(), counts.as<uint32_t>(), blocks * kBins, nullptr, s);
         if (vals)
-            radix_scatter<true><<<(unsigned)blocks, kThreads, 0, s>>>(
+            radix_scatter<true><<<(unsigned)blocks, kThreads, scatter_smem<true>(), s>>>(
                 kin, vin, n, shift, counts.as<uint32_t>(), kout, vout, unsorted);
         else
-            radix_scatter<false><<<(unsigned)blocks, kThreads, 0, s>>>(
+            radix_scatter<false><<<(unsigned)blocks, kThreads, scatter_smem<false>(), s>>>(
                 kin, nullptr, n, shift, counts.as<uint32_t>(), kout, nullptr, unsorted);
         SRDL_CHECK_LAUNCH();
         std::swap(kin, kout);
