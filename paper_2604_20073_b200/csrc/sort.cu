@@ -56,7 +56,7 @@ constexpr size_t scatter_smem() {
 }
 
 template <bool HAS_VALS>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 resident tiles per SM
     radix_scatter(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n,
                   int shift, const uint32_t *__restrict__ offsets, uint64_t *__restrict__ keys_out,
                   uint32_t *__restrict__ vals_out, const int *__restrict__ unsorted) {

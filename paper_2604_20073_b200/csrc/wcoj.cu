@@ -79,6 +79,8 @@ struct Rng {
 struct View {
     uint64_t *leaf_pref;  // [33] exclusive prefix of parent leaf lengths
     uint64_t *mid_pref;   // [33] exclusive prefix of grandparent candidate lengths
+    uint64_t *wpre;       // [33] staged root keys: wpre[0] = prefix before the window, then 32 prefixes
+    uint32_t *wroot;      // [5 * 32] staged d2, key, outer row, outer degree, inner row
     Rng *rng;             // [(D+1) * A * 2] ranges on entry of level L
     Rng *leaf;            // [32 * NL * 2] per-parent leaf ranges
     Rng *mid;             // [32 * NM * 2] per-grandparent ranges of deep atoms
@@ -107,6 +109,7 @@ struct View {
 
 __host__ __device__ inline size_t warp_bytes(uint32_t D, uint32_t A, uint32_t NL, uint32_t NM) {
     size_t b = 2 * 33 * 8;                          // prefixes
+    b += 33 * 8 + 5 * 32 * 4;                       // root-key window
     b += (size_t)(D + 1) * A * 2 * sizeof(Rng);     // rng
     b += (size_t)32 * NL * 2 * sizeof(Rng);         // leaf
     b += (size_t)32 * NM * 2 * sizeof(Rng);         // mid
@@ -126,6 +129,10 @@ __device__ __forceinline__ View make_view(unsigned char *base, uint32_t D, uint3
     p += 33 * 8;
     v.mid_pref = (uint64_t *)p;
     p += 33 * 8;
+    v.wpre = (uint64_t *)p;
+    p += 33 * 8;
+    v.wroot = (uint32_t *)p;
+    p += 5 * 32 * 4;
     v.rng = (Rng *)p;
     p += (size_t)(D + 1) * A * 2 * sizeof(Rng);
     v.leaf = (Rng *)p;
@@ -708,9 +715,12 @@ __device__ __forceinline__ void descend(const srdl_plan &P, const View &S, int L
     __syncwarp();
 }
 
+// Staged root-key window fields (S.wroot[field * 32 + j]).
+enum : uint32_t { kWD2 = 0, kWKey = 1, kWOlo = 2, kWOdeg = 3, kWIlo = 4 };
+
 // One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
 template <bool WRITE, int KIND>
-__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t k,
+__device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t j,
                          uint32_t key, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
                          Sink<WRITE> &sink) {
     const uint32_t l = lane_id();
@@ -726,11 +736,11 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
     if (mine) has0 = A.lvl_ncol[0] != 0;
     if (has0 && lo < hi) {
         if (a == P.outer && X.outer_lo) {  // single segment: rows straight from the histogram
-            lo += X.outer_lo[k];
-            hi = lo + X.outer_deg[k];
+            lo += S.wroot[kWOlo * 32 + j];
+            hi = lo + S.wroot[kWOdeg * 32 + j];
         } else if (a == P.inner && X.inner_lo) {
-            lo += X.inner_lo[k];
-            hi = lo + X.d2[k];
+            lo += S.wroot[kWIlo * 32 + j];
+            hi = lo + S.wroot[kWD2 * 32 + j];
         } else {
             Rng t{lo, hi};
             narrow_first(A, s, 0, key, t);
@@ -861,27 +871,62 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
                 else
                     hi = mid;
             }
+            // root keys are staged 32 at a time in shared memory (lane i
+            // loads entry kb + i of every work array: one coalesced load per
+            // array per window) instead of a chain of uniform global loads
+            // per key
+            const uint32_t l = lane_id();
+            uint64_t kb = lo;
+            uint32_t j = 32;  // forces the first window load
             SRDL_LOOP
-            for (uint64_t k = lo; k < K; ++k) {
-                const uint64_t start = k ? X.prefix[k - 1] : 0;
+            for (uint64_t k = lo; k < K; ++k, ++j) {
+                if (j == 32) {
+                    const uint64_t before = k == lo ? (lo ? X.prefix[lo - 1] : 0) : S.wpre[32];
+                    __syncwarp();
+                    kb = k;
+                    j = 0;
+                    const uint64_t e = kb + l;
+                    if (l == 0) S.wpre[0] = before;
+                    if (e < K) {
+                        S.wpre[1 + l] = X.prefix[e];
+                        S.wroot[kWD2 * 32 + l] = X.d2[e];
+                        S.wroot[kWKey * 32 + l] = X.keys[e];
+                        if (X.outer_lo) {
+                            S.wroot[kWOlo * 32 + l] = X.outer_lo[e];
+                            S.wroot[kWOdeg * 32 + l] = X.outer_deg[e];
+                        }
+                        if (X.inner_lo) S.wroot[kWIlo * 32 + l] = X.inner_lo[e];
+                    }
+                    __syncwarp();
+                }
+                const uint64_t start = S.wpre[j];
                 if (start >= be) break;
-                const uint64_t end = X.prefix[k];
+                const uint64_t end = S.wpre[j + 1];
                 const uint64_t u0 = (bs > start ? bs : start) - start;
                 const uint64_t u1 = (be < end ? be : end) - start;
                 if (u0 >= u1) continue;
-                const uint64_t d2 = X.d2[k];
-                const uint32_t key = X.keys[k];
-                uint64_t ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
+                const uint32_t d2 = S.wroot[kWD2 * 32 + j];
+                const uint32_t key = S.wroot[kWKey * 32 + j];
+                uint64_t ra, ca, rb, cb;
+                if (u1 < (1ull << 32)) {  // 32-bit division (the common case)
+                    const uint32_t x0 = (uint32_t)u0, x1 = (uint32_t)u1;
+                    ra = x0 / d2;
+                    ca = x0 - (uint32_t)ra * d2;
+                    rb = x1 / d2;
+                    cb = x1 - (uint32_t)rb * d2;
+                } else {
+                    ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
+                }
                 if (ra == rb) {
-                    run_rect<WRITE, KIND>(P, X, S, k, key, ra, ra + 1, ca, cb, sink);
+                    run_rect<WRITE, KIND>(P, X, S, j, key, ra, ra + 1, ca, cb, sink);
                     continue;
                 }
                 if (ca) {
-                    run_rect<WRITE, KIND>(P, X, S, k, key, ra, ra + 1, ca, d2, sink);
+                    run_rect<WRITE, KIND>(P, X, S, j, key, ra, ra + 1, ca, d2, sink);
                     ++ra;
                 }
-                if (ra < rb) run_rect<WRITE, KIND>(P, X, S, k, key, ra, rb, 0, d2, sink);
-                if (cb) run_rect<WRITE, KIND>(P, X, S, k, key, rb, rb + 1, 0, cb, sink);
+                if (ra < rb) run_rect<WRITE, KIND>(P, X, S, j, key, ra, rb, 0, d2, sink);
+                if (cb) run_rect<WRITE, KIND>(P, X, S, j, key, rb, rb + 1, 0, cb, sink);
             }
         }
         if (lane_id() == 0) {
