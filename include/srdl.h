@@ -79,6 +79,14 @@ int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, 
 
 /* reference: rowops.is_sorted_strict (rowops.py:64). *ok = 1 iff rows are
  * strictly increasing (sorted, no duplicates). */
+/* srdl_compute_delta without the host round trip: the number of rows
+ * written to `out` (capacity n) lands in *count_dev (device memory), so the
+ * engine can launch the delta of every head relation of a stratum and read
+ * all sizes back at once (reference: storage.compute_delta, storage.py:311). */
+int srdl_compute_delta_async(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                             const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,
+                             uint32_t nseg, uint32_t *const *out, uint32_t *count_dev, void *stream);
+
 int srdl_is_sorted_strict(const uint32_t *const *cols, uint32_t arity, uint64_t n, int *ok,
                           void *stream);
 
@@ -110,11 +118,24 @@ int srdl_histogram_union(const uint32_t *col, uint64_t n, const uint32_t *fkeys,
                          uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix, uint64_t *kd_out,
                          uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *ku_out, void *stream);
 
+/* srdl_histogram_union without the host round trip: (K_delta, K_union) land
+ * in k_dev[0..1] (device memory); outputs as srdl_histogram_union. */
+int srdl_histogram_union_async(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                               uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix,
+                               uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint32_t *k_dev,
+                               void *stream);
+
 /* Dense column-0 offsets from a histogram (keys[K], inclusive prefix[K]):
  * off[v] = number of rows whose column 0 is < v, for v in [0, n_ids];
  * off has n_ids + 1 entries. The CSR row index of a sorted relation. */
 int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nkeys,
                        uint32_t n_ids, uint32_t *off, void *stream);
+
+/* Fence keys of a sorted key array: fence[i] = keys[i * SRDL_FENCE] for
+ * i < ceil(n / SRDL_FENCE) (the first level of the two-level column-0 search
+ * in the WCOJ kernels; reference: the bisect in storage.narrow_segments,
+ * storage.py:122, over Histogram.keys). */
+int srdl_key_fence(const uint32_t *keys, uint64_t n, uint32_t *fence, void *stream);
 
 /* Narrow one sorted segment on its leading columns to constant values
  * (reference: executor.prepare constant narrowing, executor.py:188-206,
@@ -148,6 +169,13 @@ typedef struct {
      * column 0 == v are [doff[v], doff[v+1]) for v < dn (two loads) */
     uint32_t dn;
     const uint32_t *doff;
+    /* optional fence keys of the histogram: hfence[i] = hkeys[i * SRDL_FENCE]
+     * for i < hfn. The column-0 search first bisects this short array (it
+     * stays in L1), then one SRDL_FENCE-key block of hkeys, instead of
+     * log2(hk) dependent L2 round trips. */
+    const uint32_t *hfence;
+    uint32_t hfn;
+    uint32_t reserved;
 } srdl_atom;
 
 /* One compiled rule instance (reference: planner.JoinPlan, planner.py:53-73). */
@@ -169,6 +197,9 @@ typedef struct {
     uint32_t nmid;
     srdl_atom atom[SRDL_MAX_ATOMS];
 } srdl_plan;
+
+/* histogram keys per fence block (srdl_atom.hfence, srdl_key_fence) */
+#define SRDL_FENCE 64
 
 /* at most this many atoms may constrain the last variable of a plan */
 #define SRDL_MAX_LEAF_SPECS 6

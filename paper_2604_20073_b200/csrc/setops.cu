@@ -294,6 +294,12 @@ __global__ void combine_pairs_dev(const uint32_t *__restrict__ mk, const uint32_
     }
 }
 
+__global__ void fence_kernel(const uint32_t *__restrict__ keys, uint64_t m, uint32_t *__restrict__ fence) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        fence[i] = keys[i * SRDL_FENCE];
+}
+
 static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, uint32_t *degrees,
                                uint64_t *prefix, cudaStream_t s) {
     if (n == 0) return 0;
@@ -320,6 +326,12 @@ static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, 
 }  // namespace srdl
 
 using namespace srdl;
+
+static void histogram_union_impl(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                                 uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix,
+                                 uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *kd_out,
+                                 uint64_t *ku_out, uint32_t *k_dev, cudaStream_t s);
+
 
 extern "C" {
 
@@ -381,9 +393,36 @@ int srdl_histogram_union(const uint32_t *col, uint64_t n, const uint32_t *fkeys,
                          uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix, uint64_t *kd_out,
                          uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *ku_out, void *stream) {
     return guarded([&] {
-        cudaStream_t s = (cudaStream_t)stream;
         *kd_out = 0;
         *ku_out = 0;
+        histogram_union_impl(col, n, fkeys, fdeg, nf, dkeys, ddeg, dprefix, ukeys, udeg, uprefix, kd_out, ku_out,
+                             nullptr, (cudaStream_t)stream);
+    });
+}
+
+int srdl_histogram_union_async(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                               uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix,
+                               uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint32_t *k_dev,
+                               void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(k_dev != nullptr, "histogram_union_async needs two device count slots");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (n == 0) {
+            SRDL_CUDA(cudaMemsetAsync(k_dev, 0, 2 * sizeof(uint32_t), s));
+            return;
+        }
+        histogram_union_impl(col, n, fkeys, fdeg, nf, dkeys, ddeg, dprefix, ukeys, udeg, uprefix, nullptr, nullptr,
+                             k_dev, s);
+    });
+}
+
+}  // extern "C"
+
+static void histogram_union_impl(const uint32_t *col, uint64_t n, const uint32_t *fkeys, const uint32_t *fdeg,
+                                 uint64_t nf, uint32_t *dkeys, uint32_t *ddeg, uint64_t *dprefix,
+                                 uint32_t *ukeys, uint32_t *udeg, uint64_t *uprefix, uint64_t *kd_out,
+                                 uint64_t *ku_out, uint32_t *k_dev, cudaStream_t s) {
+    {
         if (n == 0) return;
         SRDL_REQUIRE(n + nf < (1ull << 32), "histogram_union: %llu keys exceed 2^32",
                      (unsigned long long)(n + nf));
@@ -416,11 +455,27 @@ int srdl_histogram_union(const uint32_t *col, uint64_t n, const uint32_t *fkeys,
                                                   pos.as<uint32_t>(), nf, kd, ukeys, udeg, deg64.as<uint64_t>());
         SRDL_CHECK_LAUNCH();
         inclusive_scan_u64(deg64.as<uint64_t>(), uprefix, cap, s);
+        if (k_dev) {  // asynchronous: (K_delta, K_union) stay on the device
+            SRDL_CUDA(cudaMemcpyAsync(k_dev, kd, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            SRDL_CUDA(cudaMemcpyAsync(k_dev + 1, ku, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+            return;
+        }
         uint32_t h[4] = {0, 0, 0, 0};
         SRDL_CUDA(cudaMemcpyAsync(h, kd, sizeof(h), cudaMemcpyDeviceToHost, s));
         SRDL_CUDA(cudaStreamSynchronize(s));
         *kd_out = h[0];
         *ku_out = h[2];
+    }
+}
+
+extern "C" {
+
+int srdl_key_fence(const uint32_t *keys, uint64_t n, uint32_t *fence, void *stream) {
+    return guarded([&] {
+        const uint64_t m = (n + SRDL_FENCE - 1) / SRDL_FENCE;
+        if (m == 0) return;
+        fence_kernel<<<stride_grid(m), kThreads, 0, (cudaStream_t)stream>>>(keys, m, fence);
+        SRDL_CHECK_LAUNCH();
     });
 }
 

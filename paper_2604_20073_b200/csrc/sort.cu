@@ -392,7 +392,8 @@ constexpr uint64_t kDeviceBranchRows = 1ull << 22;
 
 static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, uint64_t n,
                                   uint32_t bits, const Segs &S, uint32_t *const *out,
-                                  cudaStream_t s, bool want_count = true) {
+                                  cudaStream_t s, bool want_count = true,
+                                  uint32_t *count_dev = nullptr) {
     SRDL_REQUIRE(arity >= 1 && arity <= SRDL_MAX_COLS, "arity %u outside [1, %d]", arity,
                  SRDL_MAX_COLS);
     SRDL_REQUIRE(bits >= 1 && bits <= 32, "bits %u outside [1, 32]", bits);
@@ -405,7 +406,7 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
     Scratch keep(n * sizeof(uint32_t), s);
     Scratch total(sizeof(uint32_t) * 2, s);
     const uint32_t per_chunk = 64 / bits;
-    const bool device_branch = n <= kDeviceBranchRows;
+    const bool device_branch = n <= kDeviceBranchRows || count_dev != nullptr;
     Scratch unsorted(sizeof(int), s);
     const int *uns = nullptr;
     if (device_branch) {
@@ -470,6 +471,10 @@ static uint64_t sort_unique_minus(const uint32_t *const *cols, uint32_t arity, u
                                             dst);
         SRDL_CHECK_LAUNCH();
     }
+    if (count_dev) {  // asynchronous: the count stays on the device
+        SRDL_CUDA(cudaMemcpyAsync(count_dev, total.as<uint32_t>(), sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        return n;
+    }
     if (!want_count) return n;  // caller guarantees distinct rows: no round trip
     uint32_t cnt = 0;
     SRDL_CUDA(cudaMemcpyAsync(&cnt, total.as<uint32_t>(), sizeof(cnt), cudaMemcpyDeviceToHost, s));
@@ -508,6 +513,29 @@ int srdl_compute_delta(const uint32_t *const *cols, uint32_t arity, uint64_t n, 
             S.nseg++;
         }
         *n_out = sort_unique_minus(cols, arity, n, bits, S, out, (cudaStream_t)stream);
+    });
+}
+
+int srdl_compute_delta_async(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
+                             const uint32_t *const *const *seg_cols, const uint64_t *seg_rows,
+                             uint32_t nseg, uint32_t *const *out, uint32_t *count_dev, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(nseg <= kMaxDiffSegs, "at most %d full segments", kMaxDiffSegs);
+        SRDL_REQUIRE(count_dev != nullptr, "compute_delta_async needs a device count slot");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (n == 0) {
+            SRDL_CUDA(cudaMemsetAsync(count_dev, 0, sizeof(uint32_t), s));
+            return;
+        }
+        Segs S{};
+        S.nseg = 0;
+        for (uint32_t q = 0; q < nseg; ++q) {
+            if (seg_rows[q] == 0) continue;
+            S.seg[S.nseg] = make_cols(seg_cols[q], arity);
+            S.rows[S.nseg] = seg_rows[q];
+            S.nseg++;
+        }
+        sort_unique_minus(cols, arity, n, bits, S, out, s, false, count_dev);
     });
 }
 

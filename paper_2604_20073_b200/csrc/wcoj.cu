@@ -189,6 +189,23 @@ SRDL_SEARCH uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint3
 // distinct keys (a few MB, L2-resident) instead of the n rows.
 SRDL_SEARCH bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
     uint32_t lo = 0, hi = A.hk;
+    if (A.hfence) {  // first level: the fence keys (short, L1-resident)
+        uint32_t flo = 0, fhi = A.hfn;
+        while (flo < fhi) {
+            const uint32_t mid = (flo + fhi) >> 1;
+            if (__ldg(A.hfence + mid) <= v)
+                flo = mid + 1;
+            else
+                fhi = mid;
+        }
+        // keys[(flo-1) * F] <= v < keys[flo * F]: one block of hkeys left
+        if (flo == 0) {
+            r.hi = r.lo;
+            return true;
+        }
+        lo = (flo - 1) * SRDL_FENCE;
+        hi = min(A.hk, flo * SRDL_FENCE);
+    }
     while (lo < hi) {
         uint32_t mid = (lo + hi) >> 1;
         if (__ldg(A.hkeys + mid) < v)

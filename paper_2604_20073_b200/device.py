@@ -58,6 +58,9 @@ class AtomDesc(C.Structure):
         ("hk", C.c_uint32),
         ("dn", C.c_uint32),
         ("doff", C.c_void_p),
+        ("hfence", C.c_void_p),
+        ("hfn", C.c_uint32),
+        ("reserved", C.c_uint32),
     ]
 
 
@@ -140,6 +143,17 @@ _SIGNATURES = {
         [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
          C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
     ),
+    "srdl_compute_delta_async": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+         C.c_void_p, C.c_void_p],
+    ),
+    "srdl_histogram_union_async": (
+        C.c_int,
+        [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "srdl_key_fence": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "srdl_dense_offsets": (
         C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]
     ),
@@ -310,6 +324,41 @@ def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
     return _trim(out, got.value)
 
 
+def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: torch.Tensor) -> torch.Tensor:
+    """compute_delta into a capacity-n buffer; the row count is written to
+    count_slot (a 1-element uint32 device tensor) without a host round trip."""
+    arity, n = rows.shape
+    out = empty_rows(arity, n)
+    segs = [s for s in segments if nrows(s)]
+    if len(segs) > MAX_DIFF_SEGS:
+        raise InternalError(f"compute_delta: at most {MAX_DIFF_SEGS} segments")
+    seg_ptr_arrays = [col_ptrs(s) for s in segs]
+    seg_cols = (C.c_void_p * MAX_DIFF_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
+    seg_rows = (C.c_uint64 * MAX_DIFF_SEGS)(*[nrows(s) for s in segs])
+    check(lib().srdl_compute_delta_async(col_ptrs(rows) if n else None, arity, n, bits, seg_cols, seg_rows,
+                                         len(segs), col_ptrs(out) if n else None, count_slot.data_ptr(),
+                                         stream_handle()), "compute_delta_async")
+    return out
+
+
+def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor, k_slots: torch.Tensor):
+    """histogram_union with capacity-sized outputs; (K_delta, K_union) are
+    written to k_slots[0:2] (uint32 device tensor) without a round trip."""
+    n, nf = col.numel(), fkeys.numel()
+    d = device()
+    dk = torch.empty(n, dtype=U32, device=d)
+    dd = torch.empty(n, dtype=U32, device=d)
+    dp = torch.empty(n, dtype=U64, device=d)
+    uk = torch.empty(n + nf, dtype=U32, device=d)
+    ud = torch.empty(n + nf, dtype=U32, device=d)
+    up = torch.empty(n + nf, dtype=U64, device=d)
+    check(lib().srdl_histogram_union_async(col.data_ptr() if n else None, n, fkeys.data_ptr() if nf else None,
+                                           fdeg.data_ptr() if nf else None, nf, dk.data_ptr(), dd.data_ptr(),
+                                           dp.data_ptr(), uk.data_ptr(), ud.data_ptr(), up.data_ptr(),
+                                           k_slots.data_ptr(), stream_handle()), "histogram_union_async")
+    return (dk, dd, dp), (uk, ud, up)
+
+
 def merge(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """Sorted union of two sorted, disjoint row sets."""
     arity = a.shape[0]
@@ -395,6 +444,18 @@ def histogram_union(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor):
                                      C.byref(ku), stream_handle()), "histogram_union")
     a, b = kd.value, ku.value
     return (dk[:a], dd[:a], dp[:a]), (uk[:b], ud[:b], up[:b])
+
+
+FENCE = 64  # SRDL_FENCE
+
+
+def key_fence(keys: torch.Tensor) -> torch.Tensor:
+    """Every FENCE-th key (first level of the kernels' column-0 search)."""
+    n = keys.numel()
+    out = torch.empty(-(-n // FENCE), dtype=U32, device=device())
+    if n:
+        check(lib().srdl_key_fence(keys.data_ptr(), n, out.data_ptr(), stream_handle()), "key_fence")
+    return out
 
 
 def dense_offsets(keys, prefix, n_ids: int) -> torch.Tensor:

@@ -177,6 +177,10 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                 ad.hkeys = hist.keys.data_ptr()
                 ad.hprefix = hist.prefix.data_ptr()
                 ad.hk = hist.nkeys
+                fence = hist.fence()
+                if fence is not None:
+                    ad.hfence = fence.data_ptr()
+                    ad.hfn = fence.numel()
                 dense = prep.rels[a].dense_offsets(prep.n_ids) if prep.n_ids else None
                 if dense is not None:
                     ad.doff = dense.data_ptr()
@@ -292,6 +296,11 @@ class CountResult:
     total_dev: torch.Tensor
     ticket: torch.Tensor | None = None
     _total: int | None = None
+
+    @classmethod
+    def none(cls) -> "CountResult":
+        """A plan with no root work: nothing on the device, total 0."""
+        return cls(None, None, None, None, 0)
 
     @classmethod
     def constant(cls, n_slices: int, first: int) -> "CountResult":
@@ -423,6 +432,14 @@ class PlanExecution:
             # the count kernels of other plans, on other streams, read too
             self.prep.descriptor()
         return self.partition
+
+    def has_work(self) -> bool:
+        """False when the count pass would launch nothing useful (an empty
+        source or no root keys): the stream schedule then skips the plan
+        without touching the device."""
+        if self.plan.depth == 0:
+            return True
+        return bool(self.prep.ok) and self.partition.nkeys > 0
 
     def count(self) -> CountResult:
         self.counts = count_pass(self.plan, self.store, self.partition, self.prep)
