@@ -76,9 +76,9 @@ def _resolve(store, pa):
 class Prepared:
     """Read-only device view of one plan execution's sources."""
 
-    __slots__ = ("plan", "rels", "segs", "ok", "head_resolved", "n_ids", "_desc")
+    __slots__ = ("plan", "rels", "segs", "ok", "head_resolved", "n_ids", "_desc", "derived")
 
-    def __init__(self, plan, rels, segs, ok, head_resolved, n_ids=0):
+    def __init__(self, plan, rels, segs, ok, head_resolved, n_ids=0, derived=None):
         self.plan = plan
         self.rels = rels
         self.segs = segs  # per atom: [(rows tensor, lo, hi), ...] body first
@@ -86,6 +86,9 @@ class Prepared:
         self.head_resolved = head_resolved
         self.n_ids = n_ids  # ids are < n_ids (symbol table size)
         self._desc = None
+        # relations derived by the running stratum (their indexes change every
+        # iteration); None = unknown, treat every index as changing
+        self.derived = derived
 
     def descriptor(self) -> dev.PlanDesc:
         if self._desc is None:
@@ -93,7 +96,7 @@ class Prepared:
         return self._desc
 
 
-def prepare(plan: JoinPlan, store, interner) -> Prepared:
+def prepare(plan: JoinPlan, store, interner, derived=None) -> Prepared:
     ok = True
     rels, segs = [], []
     for pa in plan.atoms:
@@ -117,7 +120,7 @@ def prepare(plan: JoinPlan, store, interner) -> Prepared:
         if pa.negated and pa.check_level == -1 and src:
             ok = False
     head = tuple((True, x) if kind == VAR else (False, interner.intern(x)) for kind, x in plan.head_cols)
-    return Prepared(plan, rels, segs, ok, head, len(interner))
+    return Prepared(plan, rels, segs, ok, head, len(interner), derived)
 
 
 def encode_plan(prep: Prepared) -> dev.PlanDesc:
@@ -181,7 +184,8 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                 if fence is not None:
                     ad.hfence = fence.data_ptr()
                     ad.hfn = fence.numel()
-                dense = prep.rels[a].dense_offsets(prep.n_ids) if prep.n_ids else None
+                static = prep.derived is not None and pa.relation not in prep.derived
+                dense = prep.rels[a].dense_offsets(prep.n_ids, static) if prep.n_ids else None
                 if dense is not None:
                     ad.doff = dense.data_ptr()
                     ad.dn = prep.n_ids
@@ -367,7 +371,7 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
         torch.empty(n, dtype=dev.U64, device=d),
         torch.empty(n, dtype=dev.U64, device=d),
         torch.empty(1, dtype=dev.U64, device=d),
-        torch.zeros(1, dtype=torch.int32, device=d),
+        torch.empty(1, dtype=torch.int32, device=d),  # ticket: zeroed by srdl_wcoj_count
     )
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
@@ -409,12 +413,13 @@ class PlanExecution:
     """One plan's pipeline split into phases so schedulers can interleave
     the same phase of independent plans (reference executor.PlanExecution)."""
 
-    def __init__(self, plan, store, p, interner, pool=None, dist=None):
+    def __init__(self, plan, store, p, interner, pool=None, dist=None, derived=None):
         self.plan = plan
         self.store = store
         self.p = p
         self.interner = interner
         self.dist = dist
+        self.derived = derived
         self.prep = None
         self.partition = None
         self.counts = None
@@ -424,7 +429,7 @@ class PlanExecution:
         self.aux_peak = 0
 
     def histogram(self):
-        self.prep = prepare(self.plan, self.store, self.interner)
+        self.prep = prepare(self.plan, self.store, self.interner, self.derived)
         self.partition = build_partition(self.plan, self.store, self.p, self.prep, dist=self.dist)
         if self.plan.depth and self.prep.ok:
             # encode now, on the calling (main) stream: the descriptor builds
