@@ -230,6 +230,26 @@ typedef struct {
     uint32_t *bitmap;        /* optional (audit): per-output-slot write counter */
 } srdl_exec;
 
+/* Speculative output of the count pass (srdl_wcoj_count_spec). The count
+ * walk also writes every tuple into chunks of `chunk` tuples reserved from a
+ * bounded arena with one atomic per chunk; a slice's chunks are linked
+ * (slice_first, chunk_next). srdl_wcoj_gather then copies each slice's
+ * tuples to its exact offset — the same bytes, in the same order, as a
+ * second walk (srdl_wcoj_materialize) would write, without repeating the
+ * join. A slice that finds the arena full is flagged in slice_spill and
+ * re-walked by srdl_wcoj_materialize_spilled; the arena bound keeps the
+ * two-phase guarantee that allocation never exceeds a known size. */
+typedef struct {
+    uint32_t *cols[SRDL_MAX_HEAD]; /* head_arity arrays of nchunks * chunk  */
+    uint32_t nchunks;              /* arena capacity in chunks              */
+    uint32_t chunk;                /* tuples per chunk (power of two >= 32) */
+    uint32_t *cursor;              /* device: next free chunk (zeroed by count_spec) */
+    uint64_t *spills;              /* device: number of spilled slices (zeroed by count_spec) */
+    uint32_t *chunk_next;          /* device [nchunks]: next chunk of the same slice */
+    uint32_t *slice_first;         /* device [nslices]: first chunk of the slice */
+    uint32_t *slice_spill;         /* device [nslices]: 1 = re-walk the slice */
+} srdl_spec;
+
 /* reference: executor.build_partition (executor.py:246). From the outer
  * histogram (keys, degrees, inclusive prefix) and the inner histogram (may be
  * empty), write d2[K], the inclusive work prefix[K] (uint64) and, when the
@@ -247,6 +267,19 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream);
 /* reference: executor.materialize_pass (executor.py:458). Re-walks the
  * slices writing head tuples at slice_offsets; sets *error on divergence. */
 int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stream);
+
+/* Count pass that also writes the tuples speculatively (see srdl_spec);
+ * the counts, offsets and total are exactly those of srdl_wcoj_count. */
+int srdl_wcoj_count_spec(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec, void *stream);
+
+/* Copy every non-spilled slice's tuples from the arena to ex->out at its
+ * offset (after srdl_wcoj_count_spec; reference: executor.materialize_pass
+ * output layout, executor.py:458). */
+int srdl_wcoj_gather(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec, void *stream);
+
+/* srdl_wcoj_materialize restricted to the slices flagged in spec->slice_spill. */
+int srdl_wcoj_materialize_spilled(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec,
+                                  void *stream);
 
 /* ------------------------------------------------------------ multi-GPU
  * Owner of a value among `world` ranks (hash partitioning of root keys):

@@ -26,7 +26,7 @@
 //     across the warp and all lanes walk the concatenated ranges, so a leaf
 //     with short fan-out still keeps the warp full and output writes stay
 //     coalesced (the paper's "adjacent threads emit adjacent positions").
-// Count and materialize run the same code (template flag WRITE), so per-warp
+// Count and materialize run the same code (template flag MODE), so per-warp
 // counts are exact and writes land in [offset_w, offset_w + count_w).
 #include <stdlib.h>
 
@@ -67,6 +67,11 @@ __constant__ uint32_t c_merge_ratio = 16;
 // kDepth4Mid: depth 4 with a mid batch, level 1 feeds mid batches; kGeneral:
 // anything (DFS over the middle levels).
 enum Kind : int { kShallow = 0, kDepth3 = 1, kGeneral = 2, kDepth4Mid = 3 };
+
+// kCount: count only; kMaterialize: write at exact offsets (second walk);
+// kSpec: count and write speculatively into arena chunks (srdl_spec).
+enum Mode : int { kCount = 0, kMaterialize = 1, kSpec = 2 };
+constexpr uint32_t kNoChunk = 0xffffffffu;
 
 
 struct Rng {
@@ -280,38 +285,84 @@ SRDL_SEARCH uint32_t narrow_first(const srdl_atom &A, int s, int L, uint32_t v, 
 #else
 #define SRDL_STORE __device__ __forceinline__
 #endif
+// Head column h of the tuple whose leaf value is v (parent: its lane in the
+// parent batch).
+__device__ __forceinline__ uint32_t head_value(const srdl_plan &P, const View &S, uint32_t h,
+                                               uint32_t parent, uint32_t v, int leaf) {
+    const int lvl = P.head_level[h];
+    if (lvl < 0) return P.head_const[h];
+    if (lvl == leaf) return v;
+    if (lvl == leaf - 1) return S.V(leaf - 1, parent);
+    if (lvl == leaf - 2 && *S.gp_active) return S.V(leaf - 2, S.gp[parent]);
+    return S.bind[lvl];
+}
+
 SRDL_STORE void store_tuple(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t pos,
                             uint32_t parent, uint32_t v, int leaf) {
     SRDL_LOOP
     for (uint32_t h = 0; h < P.head_arity; ++h) {
-        const int lvl = P.head_level[h];
-        uint32_t val;
-        if (lvl < 0)
-            val = P.head_const[h];
-        else if (lvl == leaf)
-            val = v;
-        else if (lvl == leaf - 1)
-            val = S.V(leaf - 1, parent);
-        else if (lvl == leaf - 2 && *S.gp_active)
-            val = S.V(leaf - 2, S.gp[parent]);
-        else
-            val = S.bind[lvl];
         // streaming store (evict-first): the output is written once and
         // must not push the L2-resident input indexes out of L2
-        __stcs(X.out[h] + pos, val);
+        __stcs(X.out[h] + pos, head_value(P, S, h, parent, v, leaf));
     }
     if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
 }
 
-template <bool WRITE>
+template <int MODE>
 struct Sink {
     uint64_t n;       // tuples emitted so far in this slice (uniform)
     uint64_t base;    // write offset of this slice (materialize)
+    const srdl_spec *Q;  // speculative arena (kSpec)
+    uint32_t cur;     // current chunk of the slice (kSpec), kNoChunk = none yet
+    uint32_t fill;    // tuples in the current chunk
+    uint32_t first;   // first chunk of the slice
+    bool spill;       // arena exhausted: the slice is re-walked later
+
+    // lane 0 reserves the next arena chunk and links it after `cur`
+    __device__ __forceinline__ bool next_chunk() {
+        uint32_t c = 0;
+        if (lane_id() == 0) {
+            c = atomicAdd(Q->cursor, 1u);
+            if (c < Q->nchunks && cur != kNoChunk) Q->chunk_next[cur] = c;
+        }
+        c = __shfl_sync(kFull, c, 0);
+        if (c >= Q->nchunks) {
+            spill = true;
+            return false;
+        }
+        if (cur == kNoChunk) first = c;
+        cur = c;
+        fill = 0;
+        return true;
+    }
+
+    __device__ __forceinline__ void put(const srdl_plan &P, const View &S, uint64_t pos, uint32_t parent,
+                                        uint32_t v, int leaf) {
+        SRDL_LOOP
+        for (uint32_t h = 0; h < P.head_arity; ++h)
+            __stcs(Q->cols[h] + pos, head_value(P, S, h, parent, v, leaf));
+    }
+
     __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const View &S,
                                          bool alive, uint32_t parent, uint32_t v, int leaf) {
         const uint32_t m = __ballot_sync(kFull, alive);
-        if (WRITE && alive)
+        if (MODE == kMaterialize && alive)
             store_tuple(P, X, S, base + n + __popc(m & ((1u << lane_id()) - 1u)), parent, v, leaf);
+        if (MODE == kSpec && m && !spill) {
+            const uint32_t cnt = __popc(m), rank = __popc(m & ((1u << lane_id()) - 1u));
+            const uint32_t B = Q->chunk;
+            if (cur == kNoChunk || fill == B) next_chunk();
+            if (!spill) {
+                const uint32_t room = B - fill;
+                if (alive && rank < room) put(P, S, (uint64_t)cur * B + fill + rank, parent, v, leaf);
+                if (cnt <= room) {
+                    fill += cnt;
+                } else if (next_chunk()) {  // the rest starts the next chunk
+                    if (alive && rank >= room) put(P, S, (uint64_t)cur * B + (rank - room), parent, v, leaf);
+                    fill = cnt - room;
+                }
+            }
+        }
         n += __popc(m);
     }
 };
@@ -323,9 +374,9 @@ struct Sink {
 // min(last A, last B). Used for "heavy" parents whose lists are long and of
 // comparable length, where per-element binary search would cost
 // min(a,b)*log(max(a,b)) dependent loads against (a+b)/32 coalesced steps.
-template <bool WRITE>
+template <int MODE>
 __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t p,
-                           Sink<WRITE> &sink) {
+                           Sink<MODE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t ja = S.leaf_drv[p], jb = 1u - ja;
     const srdl_atom &A = P.atom[P.spec[leaf][ja]];
@@ -389,9 +440,9 @@ __device__ __forceinline__ uint64_t warp_prefix(uint64_t len, uint64_t *pref) {
 
 // Flattened leaf walk over the parents with len > 0 (per-lane driver range
 // lengths): prefix sum across the warp, every lane takes one (parent, row).
-template <bool WRITE>
+template <int MODE>
 __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &S, uint64_t len,
-                            Sink<WRITE> &sink) {
+                            Sink<MODE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t nls = P.nspec[leaf];
     const uint32_t l = lane_id();
@@ -445,9 +496,9 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &
 
 // Leaf level m-1 for a batch of parents (bit p of `parents` = lane p of the
 // level m-2 chunk; for m == 2 the single parent is the root rectangle).
-template <bool WRITE>
+template <int MODE>
 __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t parents,
-                           Sink<WRITE> &sink) {
+                           Sink<MODE> &sink) {
     const int leaf = (int)P.depth - 1;
     const uint32_t nls = P.nspec[leaf];
     const uint32_t l = lane_id();
@@ -496,10 +547,10 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S
         const uint32_t hv = heavy_mask & remaining;
         const uint32_t first_heavy = hv ? (uint32_t)(__ffs(hv) - 1) : 32u;
         const uint32_t run = first_heavy == 32u ? remaining : remaining & ((1u << first_heavy) - 1u);
-        if (run) flat_leaves<WRITE>(P, X, S, ((run >> l) & 1u) ? len : 0, sink);
+        if (run) flat_leaves<MODE>(P, X, S, ((run >> l) & 1u) ? len : 0, sink);
         remaining &= ~run;
         if (first_heavy < 32u) {
-            merge_pair<WRITE>(P, X, S, first_heavy, sink);
+            merge_pair<MODE>(P, X, S, first_heavy, sink);
             remaining &= ~(1u << first_heavy);
         }
     }
@@ -509,9 +560,9 @@ __device__ void leaf_batch(const srdl_plan &P, const srdl_exec &X, const View &S
 // `gps`, their deep-atom ranges in S.mid) are expanded over their level
 // m-2 candidates in flattened chunks of 32; each chunk's survivors become a
 // parent batch for the leaf. Replaces one serial descent per survivor.
-template <bool WRITE>
+template <int MODE>
 __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t gps,
-                          Sink<WRITE> &sink) {
+                          Sink<MODE> &sink) {
     const int leaf = (int)P.depth - 1, Lm = leaf - 1;
     const uint32_t l = lane_id();
     uint64_t len = 0;
@@ -596,7 +647,7 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
         }
         const uint32_t m = __ballot_sync(kFull, alive);
         __syncwarp();
-        if (m) leaf_batch<WRITE>(P, X, S, m, sink);
+        if (m) leaf_batch<MODE>(P, X, S, m, sink);
     }
     __syncwarp();
     if (l == 0) *S.gp_active = 0u;
@@ -629,9 +680,9 @@ __device__ __forceinline__ void open_level(const srdl_plan &P, const View &S, in
 }
 
 // Next 32 driver rows of level L -> filtered candidates. False when exhausted.
-template <bool WRITE, int KIND>
+template <int MODE, int KIND>
 __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S, int L,
-                           Sink<WRITE> &sink) {
+                           Sink<MODE> &sink) {
     const uint32_t l = lane_id();
     const uint32_t a = S.drv[L];
     const srdl_atom &D = P.atom[a];
@@ -709,9 +760,9 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
         S.mask[L] = (parents_level || gp_level) ? 0u : m;
     }
     __syncwarp();
-    if (parents_level && m) leaf_batch<WRITE>(P, X, S, m, sink);
+    if (parents_level && m) leaf_batch<MODE>(P, X, S, m, sink);
     if constexpr (KIND == kGeneral || KIND == kDepth4Mid) {
-        if (gp_level && m) mid_batch<WRITE>(P, X, S, m, sink);
+        if (gp_level && m) mid_batch<MODE>(P, X, S, m, sink);
     }
     return true;
 }
@@ -736,10 +787,10 @@ __device__ __forceinline__ void descend(const srdl_plan &P, const View &S, int L
 enum : uint32_t { kWD2 = 0, kWKey = 1, kWOlo = 2, kWOdeg = 3, kWIlo = 4 };
 
 // One (key, outer rows [r0,r1), inner rows [c0,c1)) rectangle.
-template <bool WRITE, int KIND>
+template <int MODE, int KIND>
 __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, uint32_t j,
                          uint32_t key, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
-                         Sink<WRITE> &sink) {
+                         Sink<MODE> &sink) {
     const uint32_t l = lane_id();
     const uint32_t a = l / SRDL_MAX_SEGS, s = l % SRDL_MAX_SEGS;
     const bool mine = a < P.natoms;
@@ -815,7 +866,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
             S.LF(0, j, q) = S.R(1, P.spec[1][j], q);
         }
         __syncwarp();
-        leaf_batch<WRITE>(P, X, S, 1u, sink);
+        leaf_batch<MODE>(P, X, S, 1u, sink);
         return;
     }
     if constexpr (KIND == kDepth3 || KIND == kDepth4Mid) {
@@ -823,7 +874,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
         // of a mid batch (depth 4): its chunks feed the flattened levels
         __syncwarp();
         open_level(P, S, 1);
-        while (load_chunk<WRITE, KIND>(P, X, S, 1, sink)) {
+        while (load_chunk<MODE, KIND>(P, X, S, 1, sink)) {
         }
     } else if constexpr (KIND == kGeneral) {
         __syncwarp();
@@ -834,7 +885,7 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
         while (true) {
             const uint32_t m = S.mask[L];
             if (m == 0) {
-                if (load_chunk<WRITE, KIND>(P, X, S, L, sink)) continue;
+                if (load_chunk<MODE, KIND>(P, X, S, L, sink)) continue;
                 if (L == 1) break;
                 --L;
                 continue;
@@ -849,9 +900,10 @@ __device__ void run_rect(const srdl_plan &P, const srdl_exec &X, const View &S, 
     }
 }
 
-template <bool WRITE, int KIND>
+template <int MODE, int KIND>
 __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
-    wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X) {
+    wcoj_kernel(const __grid_constant__ srdl_plan P, const __grid_constant__ srdl_exec X,
+                const __grid_constant__ srdl_spec Q) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t wib = threadIdx.x >> 5;
     const uint32_t NL = P.nspec[P.depth - 1] ? P.nspec[P.depth - 1] : 1;
@@ -877,7 +929,9 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
         uint64_t bs = (uint64_t)sl * step, be = bs + step;
         if (bs > T) bs = T;
         if (be > T) be = T;
-        Sink<WRITE> sink{0, WRITE ? X.slice_offsets[sl] : 0};
+        // materialize after a speculative count: only the spilled slices
+        if (MODE == kMaterialize && Q.slice_spill && !Q.slice_spill[sl]) continue;
+        Sink<MODE> sink{0, MODE == kMaterialize ? X.slice_offsets[sl] : 0, &Q, kNoChunk, 0, kNoChunk, false};
         if (bs < be) {
             // kappa: first key whose inclusive prefix exceeds bs
             uint64_t lo = 0, hi = K;
@@ -935,22 +989,27 @@ __global__ void __launch_bounds__(kJoinWarps * 32, kMinBlocks)
                     ra = u0 / d2, ca = u0 % d2, rb = u1 / d2, cb = u1 % d2;
                 }
                 if (ra == rb) {
-                    run_rect<WRITE, KIND>(P, X, S, j, key, ra, ra + 1, ca, cb, sink);
+                    run_rect<MODE, KIND>(P, X, S, j, key, ra, ra + 1, ca, cb, sink);
                     continue;
                 }
                 if (ca) {
-                    run_rect<WRITE, KIND>(P, X, S, j, key, ra, ra + 1, ca, d2, sink);
+                    run_rect<MODE, KIND>(P, X, S, j, key, ra, ra + 1, ca, d2, sink);
                     ++ra;
                 }
-                if (ra < rb) run_rect<WRITE, KIND>(P, X, S, j, key, ra, rb, 0, d2, sink);
-                if (cb) run_rect<WRITE, KIND>(P, X, S, j, key, rb, rb + 1, 0, cb, sink);
+                if (ra < rb) run_rect<MODE, KIND>(P, X, S, j, key, ra, rb, 0, d2, sink);
+                if (cb) run_rect<MODE, KIND>(P, X, S, j, key, rb, rb + 1, 0, cb, sink);
             }
         }
         if (lane_id() == 0) {
-            if (WRITE) {
+            if (MODE == kMaterialize) {
                 if (sink.n != X.slice_counts[sl]) atomicExch(X.error, 1u);
             } else {
                 X.slice_counts[sl] = sink.n;
+            }
+            if (MODE == kSpec) {
+                Q.slice_first[sl] = sink.first;
+                Q.slice_spill[sl] = sink.spill ? 1u : 0u;
+                if (sink.spill) atomicAdd((unsigned long long *)Q.spills, 1ull);
             }
         }
         __syncwarp();
@@ -972,13 +1031,13 @@ static int plan_kind(const srdl_plan *P) {
     return kGeneral;
 }
 
-template <bool WRITE, int KIND>
-static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+template <int MODE, int KIND>
+static void launch_kind(const srdl_plan *P, const srdl_exec *X, const srdl_spec *Q, cudaStream_t s) {
     const uint32_t NL = P->nspec[P->depth - 1] ? P->nspec[P->depth - 1] : 1;
     const size_t bytes = warp_bytes(P->depth, P->natoms, NL, P->nmid) * kJoinWarps;
     static bool raised = false;
     if (!raised) {  // allow up to the full 227 KB of dynamic shared memory
-        SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<WRITE, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<MODE, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024));
         raised = true;
     }
@@ -987,7 +1046,7 @@ static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) 
     // the register budget decide how many fit per SM); slices are fetched
     // dynamically, so more blocks would only queue
     int per_sm = 0;
-    SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<WRITE, KIND>, kJoinWarps * 32,
+    SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wcoj_kernel<MODE, KIND>, kJoinWarps * 32,
                                                             bytes));
     if (per_sm < 1) per_sm = 1;
     // The slice geometry (X->nwarps, nslices, min_units) comes from the
@@ -996,7 +1055,7 @@ static void launch_kind(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) 
     // the two instances (their occupancy can differ), so it must not feed
     // into the slicing.
     const unsigned blocks = (unsigned)(per_sm * sm_count());
-    wcoj_kernel<WRITE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, *X);
+    wcoj_kernel<MODE, KIND><<<blocks, kJoinWarps * 32, bytes, s>>>(*P, *X, *Q);
 }
 
 static void apply_tuning() {
@@ -1014,22 +1073,57 @@ static void apply_tuning() {
     }
 }
 
-template <bool WRITE>
-static void launch(const srdl_plan *P, const srdl_exec *X, cudaStream_t s) {
+template <int MODE>
+static void launch(const srdl_plan *P, const srdl_exec *X, const srdl_spec *Q, cudaStream_t s) {
     apply_tuning();
+    srdl_spec none{};
+    if (!Q) Q = &none;
     switch (plan_kind(P)) {
         case kShallow:
-            launch_kind<WRITE, kShallow>(P, X, s);
+            launch_kind<MODE, kShallow>(P, X, Q, s);
             break;
         case kDepth3:
-            launch_kind<WRITE, kDepth3>(P, X, s);
+            launch_kind<MODE, kDepth3>(P, X, Q, s);
             break;
         case kDepth4Mid:
-            launch_kind<WRITE, kDepth4Mid>(P, X, s);
+            launch_kind<MODE, kDepth4Mid>(P, X, Q, s);
             break;
         default:
-            launch_kind<WRITE, kGeneral>(P, X, s);
+            launch_kind<MODE, kGeneral>(P, X, Q, s);
     }
+}
+
+// Warp per slice: copy the slice's chunk chain to its exact output offset.
+__global__ void __launch_bounds__(256) gather_kernel(const srdl_exec X, const srdl_spec Q, uint32_t arity,
+                                                     uint32_t nslices) {
+    const uint32_t l = lane_id();
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t sl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sl < nslices; sl += warps) {
+        const uint64_t n = X.slice_counts[sl];
+        if (n == 0 || Q.slice_spill[sl]) continue;
+        uint64_t off = X.slice_offsets[sl];
+        uint32_t c = Q.slice_first[sl];
+        uint64_t left = n;
+        while (true) {
+            const uint32_t take = left < Q.chunk ? (uint32_t)left : Q.chunk;
+            const uint64_t src = (uint64_t)c * Q.chunk;
+            for (uint32_t h = 0; h < arity; ++h)
+                for (uint32_t i = l; i < take; i += 32) __stcs(X.out[h] + off + i, __ldcs(Q.cols[h] + src + i));
+            left -= take;
+            off += take;
+            if (left == 0) break;
+            c = Q.chunk_next[c];
+        }
+    }
+}
+
+static void check_spec(const srdl_plan *P, const srdl_spec *Q) {
+    SRDL_REQUIRE(Q != nullptr, "a speculative arena is required");
+    SRDL_REQUIRE(Q->chunk >= 32 && (Q->chunk & (Q->chunk - 1)) == 0, "chunk %u: power of two >= 32", Q->chunk);
+    SRDL_REQUIRE(Q->cursor && Q->spills && Q->slice_first && Q->slice_spill, "arena bookkeeping arrays missing");
+    SRDL_REQUIRE(Q->nchunks == 0 || Q->chunk_next, "chunk links missing");
+    for (uint32_t h = 0; h < P->head_arity && Q->nchunks; ++h)
+        SRDL_REQUIRE(Q->cols[h] != nullptr, "arena column %u missing", h);
 }
 
 static void check_plan(const srdl_plan *P, const srdl_exec *X) {
@@ -1055,9 +1149,48 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
         cudaStream_t s = (cudaStream_t)stream;
         SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
         SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
-        launch<false>(plan, ex, s);
+        launch<kCount>(plan, ex, nullptr, s);
         SRDL_CHECK_LAUNCH();
         exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
+    });
+}
+
+int srdl_wcoj_count_spec(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec, void *stream) {
+    return guarded([&] {
+        check_plan(plan, ex);
+        check_spec(plan, spec);
+        cudaStream_t s = (cudaStream_t)stream;
+        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
+        SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
+        SRDL_CUDA(cudaMemsetAsync(spec->cursor, 0, sizeof(uint32_t), s));
+        SRDL_CUDA(cudaMemsetAsync(spec->spills, 0, sizeof(uint64_t), s));
+        // slices the launch never reaches (beyond the used count) are empty
+        SRDL_CUDA(cudaMemsetAsync(spec->slice_spill, 0, ex->nslices * sizeof(uint32_t), s));
+        launch<kSpec>(plan, ex, spec, s);
+        SRDL_CHECK_LAUNCH();
+        exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
+    });
+}
+
+int srdl_wcoj_gather(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec, void *stream) {
+    return guarded([&] {
+        check_plan(plan, ex);
+        check_spec(plan, spec);
+        const unsigned blocks = (unsigned)(sm_count() * 8);
+        gather_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(*ex, *spec, plan->head_arity, ex->nslices);
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+int srdl_wcoj_materialize_spilled(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec,
+                                  void *stream) {
+    return guarded([&] {
+        check_plan(plan, ex);
+        check_spec(plan, spec);
+        cudaStream_t s = (cudaStream_t)stream;
+        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
+        launch<kMaterialize>(plan, ex, spec, s);
+        SRDL_CHECK_LAUNCH();
     });
 }
 
@@ -1066,7 +1199,7 @@ int srdl_wcoj_materialize(const srdl_plan *plan, const srdl_exec *ex, void *stre
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
         SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
-        launch<true>(plan, ex, s);
+        launch<kMaterialize>(plan, ex, nullptr, s);
         SRDL_CHECK_LAUNCH();
     });
 }

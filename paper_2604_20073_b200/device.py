@@ -64,6 +64,19 @@ class AtomDesc(C.Structure):
     ]
 
 
+class SpecDesc(C.Structure):
+    _fields_ = [
+        ("cols", C.c_void_p * MAX_HEAD),
+        ("nchunks", C.c_uint32),
+        ("chunk", C.c_uint32),
+        ("cursor", C.c_void_p),
+        ("spills", C.c_void_p),
+        ("chunk_next", C.c_void_p),
+        ("slice_first", C.c_void_p),
+        ("slice_spill", C.c_void_p),
+    ]
+
+
 class PlanDesc(C.Structure):
     _fields_ = [
         ("depth", C.c_uint32),
@@ -153,6 +166,9 @@ _SIGNATURES = {
         [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
+    "srdl_wcoj_count_spec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "srdl_wcoj_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "srdl_wcoj_materialize_spilled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "srdl_key_fence": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "srdl_dense_offsets": (
         C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]

@@ -300,6 +300,8 @@ class CountResult:
     total_dev: torch.Tensor
     ticket: torch.Tensor | None = None
     _total: int | None = None
+    spec: "SpecArena | None" = None  # speculative output of the count walk
+    spills: int | None = None  # slices the arena could not hold (host, after readback)
 
     @classmethod
     def none(cls) -> "CountResult":
@@ -357,8 +359,58 @@ def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=
     return x
 
 
-def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> CountResult:
-    """Read-only pass: exact per-slice output counts, nothing written."""
+SPEC_CHUNK = 128  # tuples per speculative arena chunk (srdl_spec.chunk)
+
+
+class SpecArena:
+    """Device arena the speculative count walk writes into (srdl_spec)."""
+
+    __slots__ = ("cols", "chunk_next", "slice_first", "slice_spill", "meta", "nchunks", "_desc")
+
+    def __init__(self, arity: int, capacity: int, nslices: int, storage: torch.Tensor | None = None):
+        """storage: a uint32 device region to carve the tuple columns and
+        chunk links from (the engine's persistent arena), else allocated."""
+        d = dev.device()
+        per_chunk = SPEC_CHUNK * arity + 1  # tuple columns + one link word
+        if storage is not None:
+            capacity = min(capacity, (storage.numel() // per_chunk) * SPEC_CHUNK)
+        self.nchunks = max(0, capacity // SPEC_CHUNK)
+        words = self.nchunks * SPEC_CHUNK
+        if storage is None:
+            storage = torch.empty(max(self.nchunks * per_chunk, 1), dtype=dev.U32, device=d)
+        self.cols = storage[:arity * words].view(arity, words)
+        self.chunk_next = storage[arity * words:arity * words + max(self.nchunks, 1)]
+        self.slice_first = torch.empty(nslices, dtype=dev.U32, device=d)
+        self.slice_spill = torch.empty(nslices, dtype=dev.U32, device=d)
+        self.meta = torch.empty(2, dtype=torch.int64, device=d)  # [spills, cursor]
+        self._desc = None
+
+    @property
+    def spills_dev(self) -> torch.Tensor:
+        return self.meta[0:1]
+
+    def descriptor(self) -> dev.SpecDesc:
+        if self._desc is None:
+            q = dev.SpecDesc()
+            for h in range(self.cols.shape[0]):
+                q.cols[h] = self.cols[h].data_ptr()
+            q.nchunks = self.nchunks
+            q.chunk = SPEC_CHUNK
+            q.spills = self.meta.data_ptr()
+            q.cursor = self.meta.data_ptr() + 8
+            q.chunk_next = self.chunk_next.data_ptr()
+            q.slice_first = self.slice_first.data_ptr()
+            q.slice_spill = self.slice_spill.data_ptr()
+            self._desc = q
+        return self._desc
+
+
+def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec_capacity=0,
+               spec_storage=None) -> CountResult:
+    """Read-only pass: exact per-slice output counts, nothing written.
+    spec_capacity > 0: the walk also writes its tuples speculatively into an
+    arena of that many tuples (srdl_wcoj_count_spec); materialize_pass then
+    gathers them instead of walking again."""
     if prep is None:
         prep = prepare(plan, store, interner)
     n = partition.nslices
@@ -375,9 +427,16 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None) -> C
     )
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
-    dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x),
-                                                                      dev.stream_handle()),
-                     input_bytes(prep) if KERNEL_EVENTS is not None else 0), "wcoj_count")
+    algo = input_bytes(prep) if KERNEL_EVENTS is not None else 0
+    if spec_capacity >= SPEC_CHUNK:
+        counts.spec = SpecArena(plan.head_arity, spec_capacity, n, spec_storage)
+        q = counts.spec.descriptor()
+        dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count_spec(
+            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()), algo), "wcoj_count_spec")
+    else:
+        dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x),
+                                                                          dev.stream_handle()), algo),
+                  "wcoj_count")
     return counts
 
 
@@ -401,9 +460,23 @@ def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep
     desc = prep.descriptor()
     x = _exec_desc(partition, counts, out_cols, error, bitmap)
     out_bytes = 4 * plan.head_arity * total  # every derived tuple written once
-    dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
-        C.byref(desc), C.byref(x), dev.stream_handle()),
-        input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize")
+    if counts.spec is not None and bitmap is None:
+        # the count walk already wrote the tuples: copy them to their offsets,
+        # and walk again only the slices the arena could not hold
+        q = counts.spec.descriptor()
+        spills = counts.spills if counts.spills is not None else int(counts.spec.spills_dev.item())
+        dev.check(_timed("wcoj_gather", lambda: dev.lib().srdl_wcoj_gather(
+            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()),
+            2 * out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_gather")
+        if spills:
+            dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize_spilled(
+                C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()),
+                input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize_spilled")
+        counts.spec = None  # release the arena
+    else:
+        dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
+            C.byref(desc), C.byref(x), dev.stream_handle()),
+            input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize")
     if own_flag and int(error.item()):
         raise InternalError(f"plan {plan.plan_id}: materialized tuple count diverged from the count pass")
     return out_cols
@@ -446,8 +519,9 @@ class PlanExecution:
             return True
         return bool(self.prep.ok) and self.partition.nkeys > 0
 
-    def count(self) -> CountResult:
-        self.counts = count_pass(self.plan, self.store, self.partition, self.prep)
+    def count(self, spec_capacity: int = 0, spec_storage=None) -> CountResult:
+        self.counts = count_pass(self.plan, self.store, self.partition, self.prep, spec_capacity=spec_capacity,
+                                 spec_storage=spec_storage)
         return self.counts
 
     def allocate(self, out=None):
