@@ -419,7 +419,8 @@ def bench_ours(args, rank, world, dist):
             "traffic": load_profile_traffic(wl.name, name),
             "algorithmic_bytes_per_launch": int(algo),
             "algorithmic_bytes_model": "4 B x columns x rows of every index segment the plan reads, once; "
-                                       "+ 4 B x head arity per derived tuple (materialize)",
+                                       "+ 4 B x head arity per derived tuple written (the speculative "
+                                       "count walk or materialize)",
             "launch_ms": round(per_launch * 1e3, 3),
             "launches_per_step": len(kern[name]) / args.steps,
             "kernel_share_of_step": round(sum(kern[name]) / sum(times), 4),

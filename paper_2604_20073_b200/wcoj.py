@@ -302,6 +302,7 @@ class CountResult:
     _total: int | None = None
     spec: "SpecArena | None" = None  # speculative output of the count walk
     spills: int | None = None  # slices the arena could not hold (host, after readback)
+    event: int | None = None  # index of the count launch in KERNEL_EVENTS (bench)
 
     @classmethod
     def none(cls) -> "CountResult":
@@ -428,6 +429,8 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
     algo = input_bytes(prep) if KERNEL_EVENTS is not None else 0
+    if KERNEL_EVENTS is not None:
+        counts.event = len(KERNEL_EVENTS)
     if spec_capacity >= SPEC_CHUNK:
         counts.spec = SpecArena(plan.head_arity, spec_capacity, n, spec_storage)
         q = counts.spec.descriptor()
@@ -465,6 +468,9 @@ def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep
         # and walk again only the slices the arena could not hold
         q = counts.spec.descriptor()
         spills = counts.spills if counts.spills is not None else int(counts.spec.spills_dev.item())
+        if KERNEL_EVENTS is not None and counts.event is not None:  # the count walk wrote the tuples
+            name, a, b, nbytes = KERNEL_EVENTS[counts.event]
+            KERNEL_EVENTS[counts.event] = (name, a, b, nbytes + out_bytes)
         dev.check(_timed("wcoj_gather", lambda: dev.lib().srdl_wcoj_gather(
             C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()),
             2 * out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_gather")

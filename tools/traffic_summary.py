@@ -28,7 +28,13 @@ def main():
         names[r[idx]] = r[ki]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for i, m in per.items():
-        name = "wcoj_materialize" if "wcoj_kernel<1" in names[i] or "wcoj_kernel<true" in names[i] else "wcoj_count"
+        k = names[i]
+        if "gather_kernel" in k:
+            name = "wcoj_gather"
+        elif "wcoj_kernel<1" in k or "wcoj_kernel<true" in k:
+            name = "wcoj_materialize"
+        else:  # wcoj_kernel<0 (count) and <2 (speculative count)
+            name = "wcoj_count"
         agg[name][0] += 1
         agg[name][1] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     out_path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
