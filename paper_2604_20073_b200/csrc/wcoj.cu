@@ -352,15 +352,15 @@ struct Sink {
             const uint32_t cnt = __popc(m), rank = __popc(m & ((1u << lane_id()) - 1u));
             const uint32_t B = Q->chunk;
             if (cur == kNoChunk || fill == B) next_chunk();
-            if (!spill) {
-                const uint32_t room = B - fill;
-                if (alive && rank < room) put(P, S, (uint64_t)cur * B + fill + rank, parent, v, leaf);
-                if (cnt <= room) {
-                    fill += cnt;
-                } else if (next_chunk()) {  // the rest starts the next chunk
-                    if (alive && rank >= room) put(P, S, (uint64_t)cur * B + (rank - room), parent, v, leaf);
-                    fill = cnt - room;
-                }
+            // the batch fits the current chunk or spills into the next one:
+            // reserve first, then every lane stores once (one store site)
+            const uint32_t c1 = cur, f1 = fill, room = B - fill;
+            const bool two = cnt > room;
+            if (!spill && (!two || next_chunk())) {
+                if (alive)
+                    put(P, S, rank < room ? (uint64_t)c1 * B + f1 + rank : (uint64_t)cur * B + (rank - room),
+                        parent, v, leaf);
+                fill = two ? cnt - room : f1 + cnt;
             }
         }
         n += __popc(m);

@@ -360,7 +360,7 @@ def _exec_desc(partition: DevicePartition, counts: CountResult, out=None, error=
     return x
 
 
-SPEC_CHUNK = 128  # tuples per speculative arena chunk (srdl_spec.chunk)
+SPEC_CHUNK = int(os.environ.get("SRDL_SPEC_CHUNK", 128))  # tuples per speculative arena chunk (srdl_spec.chunk)
 
 
 class SpecArena:
