@@ -1107,12 +1107,25 @@ __global__ void __launch_bounds__(256) gather_kernel(const srdl_exec X, const sr
         while (true) {
             const uint32_t take = left < Q.chunk ? (uint32_t)left : Q.chunk;
             const uint64_t src = (uint64_t)c * Q.chunk;
-            for (uint32_t h = 0; h < arity; ++h)
-                for (uint32_t i = l; i < take; i += 32) __stcs(X.out[h] + off + i, __ldcs(Q.cols[h] + src + i));
+            // the next link is loaded before the copy so its latency overlaps
+            const uint32_t nxt = left > take ? __ldg(Q.chunk_next + c) : 0u;
+            for (uint32_t h = 0; h < arity; ++h) {
+                const uint32_t *__restrict__ in = Q.cols[h] + src;
+                uint32_t *__restrict__ out = X.out[h] + off;
+                // four loads in flight per lane before the stores
+                for (uint32_t i = l; i < take; i += 128) {
+                    uint32_t v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = i + 32 * u < take ? __ldcs(in + i + 32 * u) : 0u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (i + 32 * u < take) __stcs(out + i + 32 * u, v[u]);
+                }
+            }
             left -= take;
             off += take;
             if (left == 0) break;
-            c = Q.chunk_next[c];
+            c = nxt;
         }
     }
 }
