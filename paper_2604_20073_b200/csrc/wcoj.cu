@@ -293,7 +293,7 @@ __device__ __forceinline__ uint32_t head_value(const srdl_plan &P, const View &S
     if (lvl < 0) return P.head_const[h];
     if (lvl == leaf) return v;
     if (lvl == leaf - 1) return S.V(leaf - 1, parent);
-    if (lvl == leaf - 2 && *S.gp_active) return S.V(leaf - 2, S.gp[parent]);
+    if (lvl == leaf - 2 && P.nmid && *S.gp_active) return S.V(leaf - 2, S.gp[parent]);
     return S.bind[lvl];
 }
 
@@ -308,6 +308,18 @@ SRDL_STORE void store_tuple(const srdl_plan &P, const srdl_exec &X, const View &
     if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
 }
 
+// Lane 0 reserves the next arena chunk and links it after `prev`; the chunk
+// id (>= nchunks: arena full) is broadcast. Out of line: once per chunk of
+// tuples, and one copy keeps the emit sites small.
+__device__ __noinline__ uint32_t reserve_chunk(const srdl_spec *Q, uint32_t prev) {
+    uint32_t c = 0;
+    if (lane_id() == 0) {
+        c = atomicAdd(Q->cursor, 1u);
+        if (c < Q->nchunks && prev != kNoChunk) Q->chunk_next[prev] = c;
+    }
+    return __shfl_sync(kFull, c, 0);
+}
+
 template <int MODE>
 struct Sink {
     uint64_t n;       // tuples emitted so far in this slice (uniform)
@@ -318,14 +330,8 @@ struct Sink {
     uint32_t first;   // first chunk of the slice
     bool spill;       // arena exhausted: the slice is re-walked later
 
-    // lane 0 reserves the next arena chunk and links it after `cur`
     __device__ __forceinline__ bool next_chunk() {
-        uint32_t c = 0;
-        if (lane_id() == 0) {
-            c = atomicAdd(Q->cursor, 1u);
-            if (c < Q->nchunks && cur != kNoChunk) Q->chunk_next[cur] = c;
-        }
-        c = __shfl_sync(kFull, c, 0);
+        const uint32_t c = reserve_chunk(Q, cur);
         if (c >= Q->nchunks) {
             spill = true;
             return false;
