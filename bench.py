@@ -213,12 +213,15 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, enabled=True):
         self.index = index
+        self.enabled = enabled
         self.proc = None
         self.lines = []
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
@@ -347,7 +350,8 @@ def bench_ours(args, rank, world, dist):
     wcoj.KERNEL_EVENTS = events
     launches0 = dev.lib().srdl_launch_count()
     times = []
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clocks:
+    mem0 = torch.cuda.memory_stats()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0)), enabled=not os.environ.get("SRDL_BENCH_NO_CLOCKS")) as clocks:
         for _ in range(args.steps):
             gc.collect()  # release the previous step's engine before timing
             flush_l2(torch, flush)
@@ -360,6 +364,9 @@ def bench_ours(args, rank, world, dist):
             end.synchronize()
             times.append(start.elapsed_time(end) / 1e3)
     launches = dev.lib().srdl_launch_count() - launches0
+    mem1 = torch.cuda.memory_stats()
+    alloc_diag = {k: int(mem1.get(k, 0) - mem0.get(k, 0)) for k in ("num_alloc_retries", "num_device_alloc",
+                                                                      "num_device_free")}
     wcoj.KERNEL_EVENTS = None
     step_s = sum(times) / len(times)
 
@@ -451,6 +458,7 @@ def bench_ours(args, rank, world, dist):
             "ms_per_step": e2e_s * 1e3,
         },
         "gpu_launches": int(launches / args.steps),
+        "allocator_timed_region": alloc_diag,
         "clocks": clocks.summary(),
         "roofline": roofline,
     }
