@@ -352,7 +352,10 @@ def bench_ours(args, rank, world, dist):
 
     # warm-up (also sizes the pinned output buffer)
     n_out = 0
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):  # same conditions as the timed steps
+        gc.collect()
+        flush_l2(torch, flush)
+        barrier()
         n_out = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
     # timed region: device events on the main stream, kernel events per launch
     events = []
@@ -367,10 +370,13 @@ def bench_ours(args, rank, world, dist):
             barrier()
             start = torch.cuda.Event(enable_timing=True)
             end = torch.cuda.Event(enable_timing=True)
+            if os.environ.get("SRDL_BENCH_GC_OFF"):  # diagnostics only
+                gc.disable()
             start.record()
             n_out = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
             end.record()
             end.synchronize()
+            gc.enable()
             times.append(start.elapsed_time(end) / 1e3)
     launches = dev.lib().srdl_launch_count() - launches0
     mem1 = torch.cuda.memory_stats()
