@@ -192,7 +192,15 @@ SRDL_SEARCH uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint3
 
 // Column-0 lookup through the index histogram: binary search over the K
 // distinct keys (a few MB, L2-resident) instead of the n rows.
-SRDL_SEARCH bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
+// Out of line unless SRDL_INLINE_HIST: the histogram path is only taken
+// for indexes without dense offsets, and one copy instead of one per
+// lookup site keeps every kernel instance ~1.2K instructions smaller.
+#ifdef SRDL_INLINE_HIST
+#define SRDL_HIST __device__ __forceinline__
+#else
+#define SRDL_HIST __device__ __noinline__
+#endif
+SRDL_HIST bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
     uint32_t lo = 0, hi = A.hk;
     if (A.hfence) {  // first level: the fence keys (short, L1-resident)
         uint32_t flo = 0, fhi = A.hfn;
@@ -308,6 +316,19 @@ SRDL_STORE void store_tuple(const srdl_plan &P, const srdl_exec &X, const View &
     if (X.bitmap) atomicAdd(X.bitmap + pos, 1u);
 }
 
+#ifdef SRDL_NOINLINE_SPEC
+#define SRDL_SPEC_PUT __device__ __noinline__
+#else
+#define SRDL_SPEC_PUT __device__ __forceinline__
+#endif
+
+// One head tuple into the speculative arena at `pos`.
+SRDL_SPEC_PUT void spec_put(const srdl_plan &P, const View &S, const srdl_spec *Q, uint64_t pos,
+                            uint32_t parent, uint32_t v, int leaf) {
+    SRDL_LOOP
+    for (uint32_t h = 0; h < P.head_arity; ++h) __stcs(Q->cols[h] + pos, head_value(P, S, h, parent, v, leaf));
+}
+
 // Lane 0 reserves the next arena chunk and links it after `prev`; the chunk
 // id (>= nchunks: arena full) is broadcast. Out of line: once per chunk of
 // tuples, and one copy keeps the emit sites small.
@@ -344,9 +365,7 @@ struct Sink {
 
     __device__ __forceinline__ void put(const srdl_plan &P, const View &S, uint64_t pos, uint32_t parent,
                                         uint32_t v, int leaf) {
-        SRDL_LOOP
-        for (uint32_t h = 0; h < P.head_arity; ++h)
-            __stcs(Q->cols[h] + pos, head_value(P, S, h, parent, v, leaf));
+        spec_put(P, S, Q, pos, parent, v, leaf);
     }
 
     __device__ __forceinline__ void emit(const srdl_plan &P, const srdl_exec &X, const View &S,
