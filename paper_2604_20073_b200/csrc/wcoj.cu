@@ -192,13 +192,13 @@ SRDL_SEARCH uint32_t ubound(const uint32_t *__restrict__ col, uint32_t lo, uint3
 
 // Column-0 lookup through the index histogram: binary search over the K
 // distinct keys (a few MB, L2-resident) instead of the n rows.
-// Out of line unless SRDL_INLINE_HIST: the histogram path is only taken
-// for indexes without dense offsets, and one copy instead of one per
-// lookup site keeps every kernel instance ~1.2K instructions smaller.
-#ifdef SRDL_INLINE_HIST
-#define SRDL_HIST __device__ __forceinline__
-#else
+// Inlined: an out-of-line copy (SRDL_NOINLINE_HIST) makes every instance
+// ~1.2K instructions smaller but measured slower on all four workloads
+// (triangle count 107 -> 112 ms, DOOP 1705 -> 1793 ms of WCOJ time).
+#ifdef SRDL_NOINLINE_HIST
 #define SRDL_HIST __device__ __noinline__
+#else
+#define SRDL_HIST __device__ __forceinline__
 #endif
 SRDL_HIST bool hist_range(const srdl_atom &A, uint32_t v, Rng &r) {
     uint32_t lo = 0, hi = A.hk;
