@@ -237,6 +237,11 @@ class ClockSampler:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._pump, daemon=True)
             self.thread.start()
+            # let nvidia-smi finish initialising (its NVML start-up competes
+            # with the first timed step otherwise): wait for its first sample
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.05)
         except OSError:
             self.proc = None
         return self

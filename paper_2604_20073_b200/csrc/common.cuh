@@ -79,6 +79,8 @@ class Scratch {
   private:
     void *ptr_ = nullptr;
     cudaStream_t stream_;
+    size_t bytes_ = 0;
+    size_t block_ = 0;
 };
 
 int sm_count();

@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -27,25 +29,66 @@ uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
 
 // ----------------------------------------------------------------- scratch
 
-static std::once_flag g_pool_once;
+// Scratch memory comes from a per-stream stack arena: every Scratch lives
+// inside one C-ABI call (RAII, strictly nested), so allocation is a pointer
+// bump and release a pop. Kernels of a later call on the same stream run
+// after the earlier call's kernels (stream order), so reusing the bytes is
+// safe; calls on other streams use their own arena. Blocks are cudaMalloc'ed
+// when a stack outgrows its current block and kept for the process — no
+// driver call per scratch buffer (cudaMallocAsync was measured to stall for
+// ~0.5 s now and then under torch's expandable segments).
+namespace {
 
-static void tune_pool() {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
-    uint64_t keep = ~0ull;  // never trim between iterations
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-}
+struct Block {
+    char *base;
+    size_t size, used;
+};
+
+struct StreamArena {
+    std::vector<Block> blocks;  // blocks[0..top] in use as a stack
+    size_t top = 0;
+};
+
+std::mutex g_arena_mu;
+std::unordered_map<cudaStream_t, StreamArena> g_arenas;
+
+constexpr size_t kAlign = 256;
+constexpr size_t kMinBlock = size_t(64) << 20;
+
+}  // namespace
 
 Scratch::Scratch(size_t bytes, cudaStream_t s) : stream_(s) {
-    std::call_once(g_pool_once, tune_pool);
     if (bytes == 0) bytes = 16;
-    SRDL_CUDA(cudaMallocAsync(&ptr_, bytes, s));
+    bytes = (bytes + kAlign - 1) & ~(kAlign - 1);
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    StreamArena &A = g_arenas[s];
+    // current block, else the next existing block with room, else a new one
+    while (A.top < A.blocks.size() && A.blocks[A.top].size - A.blocks[A.top].used < bytes) {
+        if (A.blocks[A.top].used == 0 && A.top + 1 >= A.blocks.size()) break;
+        ++A.top;
+    }
+    if (A.top >= A.blocks.size() || A.blocks[A.top].size - A.blocks[A.top].used < bytes) {
+        size_t want = bytes > kMinBlock ? bytes : kMinBlock;
+        if (!A.blocks.empty() && want < 2 * A.blocks.back().size) want = 2 * A.blocks.back().size;
+        if (want < bytes) want = bytes;
+        void *p = nullptr;
+        SRDL_CUDA(cudaMalloc(&p, want));
+        A.blocks.push_back(Block{(char *)p, want, 0});
+        A.top = A.blocks.size() - 1;
+    }
+    Block &b = A.blocks[A.top];
+    ptr_ = b.base + b.used;
+    bytes_ = bytes;
+    block_ = A.top;
+    b.used += bytes;
 }
 
 Scratch::~Scratch() {
-    if (ptr_) cudaFreeAsync(ptr_, stream_);
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    StreamArena &A = g_arenas[stream_];
+    Block &b = A.blocks[block_];
+    b.used -= bytes_;  // LIFO: this was the last allocation of its block
+    while (A.top > 0 && A.blocks[A.top].used == 0) --A.top;
 }
 
 int sm_count() {

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=12)
     ap.add_argument("--stats", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="CUPTI trace of slow prepare phases")
     args = ap.parse_args()
     raw = dev.gen_rmat(20, 16_000_000, seed=1).view(torch.int32)
     raw = raw[:, raw[0] != raw[1]].contiguous().view(torch.uint32)
@@ -36,8 +37,24 @@ def main():
         for r in ("R", "S", "T"):
             eng.load_columns(r, e)
         torch.cuda.synchronize(); t.append(time.perf_counter())
+        prof = None
+        if args.profile:
+            prof = torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU,
+                                                      torch.profiler.ProfilerActivity.CUDA])
+            prof.__enter__()
         eng.prepare_inputs()
         torch.cuda.synchronize(); t.append(time.perf_counter())
+        if prof is not None:
+            prof.__exit__(None, None, None)
+            if (t[-1] - t[-2]) * 1e3 > 60:
+                rows = {}
+                for ev in prof.events():
+                    if ev.device_type == torch.autograd.DeviceType.CPU:
+                        n, tt = rows.get(ev.name, (0, 0.0))
+                        rows[ev.name] = (n + 1, tt + ev.cpu_time_total / 1e3)
+                top = sorted(rows.items(), key=lambda kv: -kv[1][1])[:12]
+                print(json.dumps({"rep": rep, "slow_prepare_cpu_ms": {k: [n, round(v, 1)] for k, (n, v) in top}}),
+                      flush=True)
         eng.solve()
         torch.cuda.synchronize(); t.append(time.perf_counter())
         del eng
