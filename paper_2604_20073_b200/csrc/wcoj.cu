@@ -341,12 +341,6 @@ __device__ __noinline__ uint32_t reserve_chunk(const srdl_spec *Q, uint32_t prev
     return __shfl_sync(kFull, c, 0);
 }
 
-// Level L binds exactly the last column of atom A's index: under the fixed
-// prefix of the earlier levels its values are distinct (rows are unique).
-__device__ __forceinline__ bool last_col_unique(const srdl_atom &A, int L) {
-    return A.lvl_ncol[L] == 1 && A.lvl_col[L] + 1u == A.arity;
-}
-
 template <int MODE>
 struct Sink {
     uint64_t n;       // tuples emitted so far in this slice (uniform)
@@ -502,9 +496,7 @@ __device__ void flat_leaves(const srdl_plan &P, const srdl_exec &X, const View &
             }
             const uint32_t *col = D.seg[s].cols[D.lvl_col[leaf]];
             v = __ldg(col + row);
-            // the last index column under a fixed prefix holds distinct
-            // values: no run-start check (saves a dependent load)
-            alive = last_col_unique(D, leaf) || row == seg_lo || __ldg(col + row - 1) != v;
+            alive = row == seg_lo || __ldg(col + row - 1) != v;
             if (alive && s == 1 && n0) {
                 Rng t = r0;
                 alive = narrow_first(D, 0, leaf, v, t) == 0;  // already produced by segment 0
@@ -646,7 +638,7 @@ __device__ void mid_batch(const srdl_plan &P, const srdl_exec &X, const View &S,
             }
             const uint32_t *col = D.seg[s].cols[D.lvl_col[Lm]];
             v = __ldg(col + row);
-            alive = last_col_unique(D, Lm) || row == seg_lo || __ldg(col + row - 1) != v;
+            alive = row == seg_lo || __ldg(col + row - 1) != v;
             if (alive && s == 1 && n0) {
                 Rng t = r0;
                 alive = narrow_first(D, 0, Lm, v, t) == 0;
@@ -734,7 +726,7 @@ __device__ bool load_chunk(const srdl_plan &P, const srdl_exec &X, const View &S
     uint32_t v = 0;
     if (alive) {
         v = __ldg(col + row);
-        alive = last_col_unique(D, L) || row == seg.lo || __ldg(col + row - 1) != v;
+        alive = row == seg.lo || __ldg(col + row - 1) != v;
     }
     if (alive && s == 1) {
         Rng t = S.R(L, a, 0);
