@@ -48,7 +48,10 @@
 
 namespace srdl {
 
-constexpr int kJoinWarps = 4;
+#ifndef SRDL_JOIN_WARPS
+#define SRDL_JOIN_WARPS 4
+#endif
+constexpr int kJoinWarps = SRDL_JOIN_WARPS;  // warps per CTA (each runs its own slices)
 #ifndef SRDL_MIN_BLOCKS
 #define SRDL_MIN_BLOCKS 8
 #endif
