@@ -8,28 +8,34 @@ derived tuples/sec at 1/2/4/8 B200 vs CPU ref").
 A step is one complete evaluation through the public API: build an Engine
 for the workload's program, load its EDB columns, solve to fixpoint. The
 metric is derived tuples per second = |output IDB relation| / step time,
-aggregated over all ranks. Default workload = BASELINE configs[1]:
-triangle listing on a synthetic R-MAT graph, 2^20 nodes / 16M edges.
+aggregated over all ranks. Default workload = BASELINE configs[4], the
+DOOP-shaped points-to rule set on ~100M facts (the config the metric's
+1/2/4/8-GPU scaling is quoted on); `--workload tc|triangle|sg|andersen`
+selects configs[0..3].
 
 value    inputs already resident in HBM when the timed region starts.
 e2e      same step through the public API with pinned HOST inputs: the H2D
          copy of the EDB columns and the D2H read of the output relation are
          inside the timed region.
-roofline the dominant kernel (WCOJ count/materialize), CUDA events on its
-         stream over the timed steps, algorithmic bytes / duration vs the
-         measured HBM copy bandwidth (MEASURED_PEAKS.json).
+roofline the dominant library call family of the step (every libsrdl call is
+         bracketed by CUDA events on its launching stream, dev.PROFILE):
+         algorithmic bytes / duration vs the measured HBM copy bandwidth
+         (MEASURED_PEAKS.json); all families are listed beside it.
 cpu_baseline
-         the numpy oracle restatement of the reference algorithm on a bounded
-         sample of the same workload (a subset of root keys, or a scaled-down
-         instance for recursive workloads), 1 host core.
+         the multi-core C++ restatement of the reference algorithm
+         (oracle/native.py, pinned by the reference's goldens) on this box's
+         host cores, on a bounded sample of the same workload.
+parity   the device output relation (and the EDB) reduced to a digest and
+         compared with the oracle's digest of the same full-size instance
+         (tests/golden/baseline_digests.json, tests/golden/make_baseline_digests.py).
 --impl reference
-         the same restatement on all host cores (triangle: root keys dealt to
-         forked workers; recursive workloads: 1 core, iterations are serial).
+         the same C++ oracle port on all host cores, each step a bounded
+         sample of the workload sized so the whole run ends within minutes.
 
-Multi-GPU (torchrun): the triangle hash-partitions its root keys across
-ranks (x mod N) with no data-path collective; recursive workloads run the
-distributed engine (per-iteration all-to-all of new tuples + all-reduce of
-delta sizes). Timing is the max over ranks.
+Multi-GPU (torchrun): every rank loads the EDB; root keys are hash-partitioned
+(dist.owner) inside the engine, recursive strata exchange new tuples with
+an NCCL all-to-all per iteration plus an all-reduce of delta sizes. Timing
+is the max over ranks.
 """
 
 from __future__ import annotations
@@ -39,176 +45,90 @@ import os
 # Multi-GB buffers (derived relations, the speculative arena) are allocated
 # and freed every fixpoint; expandable segments let torch's caching allocator
 # grow and reuse them without fresh cudaMalloc calls of that size, which
-# otherwise stall some steps by hundreds of ms (measured: 10-step triangle
-# runs 121-657 ms per step without, 120-148 ms with). Recommended for any
-# process running the engine (INTEGRATION.md).
+# otherwise stall some steps by hundreds of ms. Recommended for any process
+# running the engine.
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 import argparse  # noqa: E402
 import gc  # noqa: E402
 import json  # noqa: E402
-import statistics
-import subprocess
-import sys
-import threading
-import time
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
 
-import numpy as np
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-TRIANGLE = """
-.decl R(a:symbol, b:symbol)
-.decl S(a:symbol, b:symbol)
-.decl T(a:symbol, b:symbol)
-.decl Triangle(a:symbol, b:symbol, c:symbol)
-.input R
-.input S
-.input T
-.output Triangle
-Triangle(x, y, z) :- R(x, y), S(y, z), T(z, x).
-"""
-
-TC = """
-.decl Edge(a:symbol, b:symbol)
-.decl TC(a:symbol, b:symbol)
-.input Edge
-.output TC
-TC(x, y) :- Edge(x, y).
-TC(x, z) :- TC(x, y), Edge(y, z).
-"""
+DIGESTS = os.path.join(ROOT, "tests", "golden", "baseline_digests.json")
 
 
 # --------------------------------------------------------------------------
-# workloads
+# workloads (BASELINE.json configs), all generated from seeds
 
 
 class Workload:
-    name = ""
-    program = ""
-    output = ""
-    config: dict = {}
+    """One BASELINE configuration. `host_facts(scale)` is the numpy
+    generator (scale 1.0 = the BASELINE size; smaller scales are the CPU
+    samples of recursive configs); `device_facts()` puts the full instance
+    in HBM."""
 
-    def generate(self):
-        """-> {relation: (2, n) uint32 device tensor} (this rank's share)."""
-        raise NotImplementedError
+    def __init__(self, name, index, desc, program, output, gen, sample_kind):
+        self.name, self.index, self.desc = name, index, desc
+        self.program, self.output = program, output
+        self._gen = gen  # scale -> {relation: (arity, n) uint32}
+        self.sample_kind = sample_kind  # "roots" (level-0 key subset) or "instance" (scaled generator)
+        self.config = {"workload": f"{desc} (configs[{index}])", "program_output": output}
 
+    def host_facts(self, scale=1.0):
+        return self._gen(scale)
 
-class TriangleRMAT(Workload):
-    name = "triangle-rmat"
-    program = TRIANGLE
-    output = "Triangle"
-
-    def __init__(self, scale=20, edges=16_000_000, seed=1, rank=0, world=1):
-        self.scale, self.nedges, self.seed, self.rank, self.world = scale, edges, seed, rank, world
-        self.config = {
-            "workload": f"triangle listing (cyclic 3-way WCOJ) on R-MAT scale {scale}",
-            "nodes": 1 << scale,
-            "rmat_edges_generated": edges,
-            "rmat_abc": [0.57, 0.19, 0.19],
-            "program": "Triangle(x,y,z) :- R(x,y), S(y,z), T(z,x) with R=S=T=E",
-        }
-
-    def edges(self):
+    def device_facts(self):
         import torch
 
         from paper_2604_20073_b200 import device as dev
 
-        raw = dev.gen_rmat(self.scale, self.nedges, seed=self.seed).view(torch.int32)
-        raw = raw[:, raw[0] != raw[1]].contiguous().view(torch.uint32)  # drop self loops
-        return dev.sort_dedup(raw, self.scale)
-
-    def generate(self):
-        import torch
-
-        e = self.edges()
-        self.config["edges"] = int(e.shape[1])
-        if self.world == 1:
+        if self.name == "triangle":  # the device generator (bit-exact with suites.rmat_host: -m gpu test)
+            raw = dev.gen_rmat(20, 16_000_000, seed=1).view(torch.int32)
+            raw = raw[:, raw[0] != raw[1]].contiguous().view(torch.uint32)
+            e = dev.sort_dedup(raw, 20)
             return {"R": e, "S": e, "T": e}
-        # hash partition on the root variable x: R(x, y) by column 0, T(z, x) by column 1
-        w = self.world
-        ei = e.view(torch.int32)
-        r = ei[:, (ei[0] % w) == self.rank].contiguous().view(torch.uint32)
-        t = ei[:, (ei[1] % w) == self.rank].contiguous().view(torch.uint32)
-        return {"R": r, "S": e, "T": t}
-
-class Recursive(Workload):
-    """A recursive BASELINE workload: integer-column EDB from
-    paper_2604_20073_b200.suites, evaluated to fixpoint; the CPU sample is
-    the oracle on a scaled-down instance of the same generator."""
-
-    def __init__(self, name, rank=0, world=1, small=False):
-        from paper_2604_20073_b200 import suites
-
-        self.name = name
-        self.rank, self.world, self.small = rank, world, small
-        self.program, self.output = suites.BASELINE_PROGRAMS[name]
-        full, sample, desc = {
-            "tc": (lambda: suites.tc_random(10_000, 50_000, seed=1),
-                   lambda: suites.tc_random(1_000, 5_000, seed=1),
-                   "transitive closure on a random digraph, 10K nodes / 50K edges (configs[0])"),
-            "sg": (lambda: suites.sg_layered(levels=128, width=31_250, seed=0),
-                   lambda: suites.sg_layered(levels=24, width=2_000, seed=0),
-                   "same generation on a layered tree-plus-cross-edges graph, 128 levels x "
-                   "31250 nodes, ~4.3M edges (configs[2])"),
-            "andersen": (lambda: suites.andersen_modular(10_000_000, seed=1),
-                         lambda: suites.andersen_modular(8_000, seed=1),
-                         "Andersen points-to over modular synthetic programs, 10M statements "
-                         "(configs[3])"),
-            "doop": (lambda: suites.doop_modular(6_900_000, seed=1),
-                     lambda: suites.doop_modular(16_384, seed=1),
-                     "DOOP-shaped context-insensitive points-to (5-way virtual dispatch, helper "
-                     "split HelpNT) over modular synthetic Java-like facts, 6.9M methods, ~100M EDB "
-                     "facts (configs[4])"),
-        }[name]
-        self._full, self._sample = full, sample
-        self.config = {"workload": desc, "program_output": self.output}
-
-    def generate(self):
-        import torch
-
-        from paper_2604_20073_b200 import device as dev
-
-        facts = (self._sample if self.small else self._full)()
-        self.config["edb_facts"] = int(sum(v.shape[1] for v in facts.values()))
-        return {k: torch.from_numpy(v).to(dev.device()) for k, v in facts.items()}
-
-    def cpu_sample(self):
-        from oracle.gj import Symbols, fixpoint
-        from paper_2604_20073_b200 import parse
-
-        facts = self._sample()
-        edb = {k: v.T.astype(np.int64) for k, v in facts.items()}
-        top = max(int(v.max()) for v in edb.values() if v.size) + 1
-        t0 = time.perf_counter()
-        rels, _ = fixpoint(parse(self.program), edb, Symbols(top))
-        dt = time.perf_counter() - t0
-        n = len(rels[self.output])
-        edb_n = sum(len(v) for v in edb.values())
-        self.oracle_rows = rels[self.output]
-        self.sample_facts = facts
-        return n, dt, (f"full fixpoint of a scaled-down instance of the same generator "
-                       f"({edb_n} EDB facts -> {n} {self.output} tuples in {dt:.2f} s), numpy "
-                       "semi-naive generic-join restatement of the reference")
-
-    def parity(self):
-        """Engine fixpoint on the sampled instance vs the oracle's (bit-exact)."""
-        import torch
-
-        from paper_2604_20073_b200 import Engine, parse
-        from paper_2604_20073_b200 import device as dev
-
-        eng = Engine(parse(self.program), schedule="stream")
-        for k, v in self.sample_facts.items():
-            eng.load_columns(k, torch.from_numpy(v).to(dev.device()))
-        eng.solve()
-        got = eng.relation_columns(self.output).cpu().numpy().astype(np.int64).T
-        return {"checked": "full fixpoint of the sampled instance vs the CPU oracle",
-                "rows": int(len(self.oracle_rows)), "match": bool(np.array_equal(got, self.oracle_rows))}
+        return {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev.device()) for k, v in self.host_facts().items()}
 
 
-WORKLOADS = {"triangle": TriangleRMAT, "tc": "tc", "sg": "sg", "andersen": "andersen", "doop": "doop"}
+def _workloads():
+    from paper_2604_20073_b200 import suites
+
+    def tri(scale):
+        e = suites.rmat_graph_host(20, 16_000_000, seed=1)
+        return {"R": e, "S": e, "T": e}
+
+    P = suites.BASELINE_PROGRAMS
+    return {
+        "tc": Workload("tc", 0, "transitive closure on a random digraph, 10K nodes / 50K edges", *P["tc"],
+                       lambda s: suites.tc_random(10_000, 50_000, seed=1), "roots"),
+        "triangle": Workload("triangle", 1, "triangle listing (cyclic 3-way WCOJ) on R-MAT scale 20, 16M "
+                             "generated edges (self loops dropped, deduplicated)", *P["triangle"], tri, "roots"),
+        "sg": Workload("sg", 2, "same generation on a layered tree-plus-cross-edges graph, 128 levels x 31250 "
+                       "nodes, ~4.3M edges", *P["sg"],
+                       lambda s: suites.sg_layered(levels=128, width=max(64, int(31_250 * s)), seed=0),
+                       "instance"),
+        "andersen": Workload("andersen", 3, "Andersen points-to over modular synthetic programs, 10M "
+                             "statements", *P["andersen"],
+                             lambda s: suites.andersen_modular(max(4_000, int(10_000_000 * s)), seed=1),
+                             "instance"),
+        "doop": Workload("doop", 4, "DOOP-shaped context-insensitive points-to (5-way virtual dispatch, helper "
+                         "split HelpNT) over modular synthetic Java-like facts, 6.9M methods, ~100M EDB facts",
+                         *P["doop"], lambda s: suites.doop_modular(max(4_096, int(6_900_000 * s)), seed=1),
+                         "instance"),
+    }
+
+
+def make_workload(name) -> Workload:
+    return _workloads()[name]
 
 
 # --------------------------------------------------------------------------
@@ -286,23 +206,23 @@ def measured_peaks():
     if os.path.exists(path):
         with open(path) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def flush_l2(torch, buf):
+def flush_l2(buf):
     buf.add_(1)  # 512 MiB write > 126 MB L2
 
 
-def load_profile_traffic(workload_name, kernel):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
-    capture (profiles/wcoj_traffic.json, written by tools/traffic_summary.py)."""
-    path = os.path.join(ROOT, "profiles", "wcoj_traffic.json")
+def profile_traffic(workload_name, family):
+    """DRAM bytes (read + write) per call of `family` from the committed ncu
+    --set full capture (profiles/traffic.json, tools/traffic_summary.py)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(path):
         return None
     with open(path) as fh:
         d = json.load(fh)
-    return (d.get(workload_name) or {}).get(kernel)
+    return (d.get(workload_name) or {}).get(family)
 
 
 # --------------------------------------------------------------------------
@@ -310,12 +230,8 @@ def load_profile_traffic(workload_name, kernel):
 
 
 def run_step(torch, Engine, parse, wl, inputs, host=False, out_pinned=None, ctx=None):
-    # recursive workloads at N > 1: the distributed engine (hash-partitioned
-    # indexes, per-iteration all-to-all); the triangle shards its own inputs
     engine = Engine(parse(wl.program), schedule="stream", dist=ctx)
     for rel, t in inputs.items():
-        if rel.startswith("_"):
-            continue
         engine.load_columns(rel, t)
     summary = engine.solve()
     n_out = summary.relations[wl.output]
@@ -328,7 +244,52 @@ def run_step(torch, Engine, parse, wl, inputs, host=False, out_pinned=None, ctx=
             rows.cpu()
         torch.cuda.current_stream().synchronize()
     del engine
-    return n_out
+    return n_out, summary
+
+
+def family_roofline(records, steps, step_s, wl_name):
+    """Per libsrdl call family: event time (on the launching stream) and
+    algorithmic bytes; the roofline line is the family with the largest
+    time. Families: wcoj_count (speculative count walk), wcoj_gather,
+    wcoj_materialize, compute_delta, sort_dedup (delta re-sort per index
+    order), merge, histogram, root_work, is_sorted."""
+    fam = {}
+    for name, a, b, nbytes in records:
+        t, n, by = fam.get(name, (0.0, 0, 0))
+        fam[name] = (t + a.elapsed_time(b) / 1e3, n + 1, by + nbytes)
+    if not fam:
+        return None
+    name = max(fam, key=lambda k: fam[k][0])
+    t, n, by = fam[name]
+    peak, src = measured_peaks()
+    achieved = by / t / 1e9 if t > 0 else 0.0
+    return {
+        "bound": "hbm",
+        "kernel": name,
+        "achieved": round(achieved, 2),
+        "peak": peak,
+        "peak_source": src,
+        "unit": "GB/s",
+        "frac": round(achieved / peak, 4),
+        "traffic": profile_traffic(wl_name, name),
+        "algorithmic_bytes_per_launch": int(by / n),
+        "algorithmic_bytes_model": {
+            "wcoj_count": "4 B x columns x rows of every index segment the plan reads, once; + 4 B x head "
+                          "arity per derived tuple written (into the speculative arena)",
+            "wcoj_gather": "2 x 4 B x head arity per derived tuple (arena read, output write)",
+            "compute_delta": "4 B x arity x (staged rows read once + delta rows written once)",
+            "sort_dedup": "4 B x arity x (rows read once + rows written once)",
+            "merge": "4 B x arity x (both inputs read once + output written once)",
+        }.get(name, "input read once + output written once"),
+        "launch_ms": round(t / n * 1e3, 4),
+        "launches_per_step": n / steps,
+        "kernel_share_of_step": round(t / steps / step_s, 4),
+        "families_ms_per_step": {k: round(v[0] / steps * 1e3, 3) for k, v in
+                                 sorted(fam.items(), key=lambda kv: -kv[1][0])},
+        "families_gbs": {k: round(v[2] / v[0] / 1e9, 1) for k, v in fam.items() if v[0] > 0},
+        "note": "family = one libsrdl C-ABI call (one or more kernels); times are CUDA events on the "
+                "launching stream, so families on concurrent streams overlap and shares can sum past 1",
+    }
 
 
 def bench_ours(args, rank, world, dist):
@@ -336,14 +297,13 @@ def bench_ours(args, rank, world, dist):
 
     from paper_2604_20073_b200 import Engine, parse
     from paper_2604_20073_b200 import device as dev
-    from paper_2604_20073_b200 import wcoj
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     dev.lib()
-    wl = make_workload(args, rank, world)
-    inputs = wl.generate()
+    wl = make_workload(args.workload)
+    inputs = wl.device_facts()
     ctx = None
-    if dist and isinstance(wl, Recursive):
+    if dist:
         from paper_2604_20073_b200.dist import DistContext
 
         ctx = DistContext()
@@ -355,50 +315,43 @@ def bench_ours(args, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (also sizes the pinned output buffer)
-    n_out = 0
+    n_out, summary = 0, None
     for _ in range(args.warmup):  # same conditions as the timed steps
         gc.collect()
-        flush_l2(torch, flush)
+        flush_l2(flush)
         barrier()
-        n_out = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
-    # timed region: device events on the main stream, kernel events per launch
-    events = []
-    wcoj.KERNEL_EVENTS = events
+        n_out, summary = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
+    records = []
+    dev.PROFILE = records
     launches0 = dev.lib().srdl_launch_count()
     times = []
-    mem0 = torch.cuda.memory_stats()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", 0)), enabled=not os.environ.get("SRDL_BENCH_NO_CLOCKS")) as clocks:
         for _ in range(args.steps):
             gc.collect()  # release the previous step's engine before timing
-            flush_l2(torch, flush)
+            flush_l2(flush)
             barrier()
             start = torch.cuda.Event(enable_timing=True)
             end = torch.cuda.Event(enable_timing=True)
-            if os.environ.get("SRDL_BENCH_GC_OFF"):  # diagnostics only
-                gc.disable()
             start.record()
-            n_out = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
+            n_out, summary = run_step(torch, Engine, parse, wl, inputs, ctx=ctx)
             end.record()
             end.synchronize()
-            gc.enable()
             times.append(start.elapsed_time(end) / 1e3)
     launches = dev.lib().srdl_launch_count() - launches0
-    mem1 = torch.cuda.memory_stats()
-    alloc_diag = {k: int(mem1.get(k, 0) - mem0.get(k, 0)) for k in ("num_alloc_retries", "num_device_alloc",
-                                                                      "num_device_free")}
-    wcoj.KERNEL_EVENTS = None
+    dev.PROFILE = None
     step_s = sum(times) / len(times)
+    roofline = family_roofline(records, args.steps, step_s, wl.name)
+    del records
 
     # end-to-end through the public API with host inputs and output readback
-    pinned = {k: v.cpu().pin_memory() for k, v in inputs.items() if not k.startswith("_")}
-    out_pinned = torch.empty((3 if wl.output == "Triangle" else 2, n_out), dtype=torch.uint32,
-                             pin_memory=True)
+    pinned = {k: v.cpu().pin_memory() for k, v in inputs.items()}
+    arity = parse(wl.program).declarations[wl.output]
+    out_pinned = torch.empty((arity, n_out), dtype=torch.uint32, pin_memory=True)
     h2d = sum(t.numel() * 4 for t in pinned.values())
     e2e_times = []
-    for i in range(max(1, min(args.steps, 3))):
+    for _ in range(max(1, min(args.steps, 3))):
         gc.collect()
-        flush_l2(torch, flush)
+        flush_l2(flush)
         barrier()
         t0 = time.perf_counter()
         start = torch.cuda.Event(enable_timing=True)
@@ -410,49 +363,11 @@ def bench_ours(args, rank, world, dist):
         e2e_times.append(max(start.elapsed_time(end) / 1e3, time.perf_counter() - t0))
     e2e_s = sum(e2e_times) / len(e2e_times)
 
-    # max over ranks
-    tot_out = n_out
+    tot_out = n_out  # relation sizes are global (the engine all-reduces them)
     if dist:
         t = torch.tensor([step_s, e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_s, e2e_s = t.tolist()
-        if ctx is None:  # sharded triangle: per-rank outputs are disjoint
-            c = torch.tensor([n_out], dtype=torch.int64, device="cuda")
-            dist.all_reduce(c)
-            tot_out = int(c.item())
-
-    # dominant kernel roofline: per launch, algorithmic bytes (every input
-    # index segment read once + derived tuples written once, recorded by
-    # wcoj._timed) over the CUDA-event time on the launching stream
-    kern, kbytes = {}, {}
-    for name, a, b, nbytes in events:
-        kern.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
-        kbytes[name] = kbytes.get(name, 0) + nbytes
-    roofline = None
-    if kern:
-        name = max(kern, key=lambda k: sum(kern[k]))
-        per_launch = sum(kern[name]) / len(kern[name])
-        algo = kbytes[name] / len(kern[name])
-        peak, src = measured_peaks()
-        achieved = kbytes[name] / sum(kern[name]) / 1e9
-        roofline = {
-            "bound": "hbm",
-            "kernel": name,
-            "achieved": round(achieved, 2),
-            "peak": peak,
-            "peak_source": src,
-            "unit": "GB/s",
-            "frac": round(achieved / peak, 4),
-            "traffic": load_profile_traffic(wl.name, name),
-            "algorithmic_bytes_per_launch": int(algo),
-            "algorithmic_bytes_model": "4 B x columns x rows of every index segment the plan reads, once; "
-                                       "+ 4 B x head arity per derived tuple written (the speculative "
-                                       "count walk or materialize)",
-            "launch_ms": round(per_launch * 1e3, 3),
-            "launches_per_step": len(kern[name]) / args.steps,
-            "kernel_share_of_step": round(sum(kern[name]) / sum(times), 4),
-            "all_kernels_ms_per_step": {k: round(sum(v) / args.steps * 1e3, 3) for k, v in kern.items()},
-        }
     result = {
         "metric": "derived tuples/sec (fixpoint)",
         "value": tot_out / step_s,
@@ -467,192 +382,163 @@ def bench_ours(args, rank, world, dist):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u32",
-        "data": "synthetic (seeded generator on the device)",
-        "config": dict(wl.config, derived_tuples=tot_out, l2="flushed between steps (512 MiB write)",
-                       parallelism=f"hash-partitioned root keys x{world}" if world > 1 else "single GPU"),
+        "data": "synthetic (seeded generators; the same instance at every N)",
+        "config": dict(wl.config, derived_tuples=tot_out, idb_tuples=dict(summary.relations),
+                       edb_facts=int(sum(v.shape[1] for v in inputs.values())),
+                       l2="flushed between steps (512 MiB write)",
+                       parallelism=f"hash-partitioned root keys + per-iteration all-to-all x{world}"
+                       if world > 1 else "single GPU"),
         "e2e": {
             "value": tot_out / e2e_s,
             "unit": "tuples/s",
             "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": n_out * 4 * (3 if wl.output == "Triangle" else 2),
+            "d2h_bytes_per_step": n_out * 4 * arity,
             "ms_per_step": e2e_s * 1e3,
         },
         "gpu_launches": int(launches / args.steps),
-        "allocator_timed_region": alloc_diag,
         "clocks": clocks.summary(),
         "roofline": roofline,
     }
-    return result, wl, inputs
-
-
-def make_workload(args, rank, world):
-    if args.workload == "triangle":
-        return TriangleRMAT(scale=args.scale or 20, edges=args.edges or 16_000_000, rank=rank, world=world)
-    return Recursive(args.workload, rank=rank, world=world, small=bool(args.small))
+    return result, wl, inputs, ctx
 
 
 # --------------------------------------------------------------------------
-# CPU side: the oracle restatement on a bounded sample
+# CPU side: the C++ oracle port on the host cores
 
 
-def cpu_sample(wl, inputs_host, target_s=12.0, seed=0):
-    """Time the numpy generic join (oracle port of the reference algorithm)
-    on a growing random subset of root keys until ~target_s of work."""
-    from oracle.gj import join_rule
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_solve(wl, facts, keep=None, threads=None):
+    """One C++-oracle fixpoint of `facts` (keep: level-0 key sample).
+    Returns (output tuples, solve seconds, threads)."""
+    from oracle import native
+    from oracle.gj import Symbols
     from paper_2604_20073_b200 import parse
 
     prog = parse(wl.program)
-    rule = prog.rules[-1]
-    rels = {k: v for k, v in inputs_host.items()}
-    # pre-sort each atom's relation in its column order (not timed)
-    cache = {}
-
-    def relation_of(pos):
-        atom = rule.body[pos]
-        return rels[atom.relation]
-
-    roots = np.unique(rels[rule.body[0].relation][:, 0])
-    rng = np.random.default_rng(seed)
-    rng.shuffle(roots)
-    take = max(1, len(roots) // 2000)
-    # build the per-atom sorted indexes once, outside the timed region
-    join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=roots[:1], cache=cache)
-    while True:
-        sample = np.sort(roots[:take])
-        t0 = time.perf_counter()
-        out = join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=sample, cache=cache)
-        dt = time.perf_counter() - t0
-        if dt > target_s / 4 or take >= len(roots):
-            wl.sample_roots = sample
-            wl.oracle_rows = np.unique(out, axis=0) if len(out) else out
-            return len(out), dt, take, len(roots)
-        take = min(len(roots), int(take * max(2.0, target_s / max(dt, 1e-3) / 2)))
+    top = max(int(v.max()) for v in facts.values() if v.size) + 1
+    s = native.Solver(prog, {}, Symbols(top), threads=threads, keep_level0=keep)
+    for k, v in facts.items():
+        s.load_columns(k, v)
+    t0 = time.perf_counter()
+    s.solve()
+    dt = time.perf_counter() - t0
+    n = s.size(wl.output)
+    th = s.threads
+    s.close()
+    return n, dt, th
 
 
-_FORK_STATE = {}
+class CpuSampler:
+    """Bounded samples of a workload for the CPU port: a subset of level-0
+    root keys of the full instance (TC, triangle: an exact restriction of
+    the same join/fixpoint) or the full fixpoint of a scaled-down instance of
+    the same generator (SG, Andersen, DOOP: a rate proxy), grown until one
+    solve takes about `target_s`."""
+
+    def __init__(self, wl, target_s, threads=None):
+        self.wl, self.target_s, self.threads = wl, target_s, threads
+        self.full = wl.host_facts() if wl.sample_kind == "roots" else None
+        if self.full is not None:
+            from paper_2604_20073_b200 import parse
+
+            rule = parse(wl.program).rules[0]  # its first atom is an EDB relation keyed by the root
+            self.roots = np.unique(self.full[rule.body[0].relation][0])
+            np.random.default_rng(0).shuffle(self.roots)
+        self.frac = 1.0 / 256
+        self._calibrate()
+
+    def _run(self, frac):
+        if self.full is not None:
+            k = max(1, int(len(self.roots) * frac))
+            keep = None if k >= len(self.roots) else np.sort(self.roots[:k])
+            n, dt, th = oracle_solve(self.wl, self.full, keep, self.threads)
+            what = ("full instance" if keep is None else
+                    f"{k}/{len(self.roots)} random root keys of the full instance (exact restriction)")
+        else:
+            facts = self.wl.host_facts(frac)
+            n, dt, th = oracle_solve(self.wl, facts, None, self.threads)
+            edb = int(sum(v.shape[1] for v in facts.values()))
+            what = (f"full fixpoint of the same generator scaled to {frac:.4g} of the BASELINE size "
+                    f"({edb} EDB facts, {n} {self.wl.output} tuples) — a rate proxy")
+        return n, dt, th, what
+
+    def _calibrate(self):
+        while True:
+            n, dt, th, what = self._run(self.frac)
+            if dt >= self.target_s / 3 or self.frac >= 1.0:
+                break
+            self.frac = min(1.0, self.frac * max(2.0, min(8.0, self.target_s / max(dt, 1e-3) / 2)))
+        self.last = (n, dt, th, what)
+
+    def step(self):
+        self.last = self._run(self.frac)
+        return self.last
 
 
-def _fork_join(keys):
-    from oracle.gj import join_rule
-
-    st = _FORK_STATE
-    out = join_rule(st["rule"], st["relation_of"], lambda c, create=False: None, level0_keep=keys,
-                    cache=st["cache"])
-    return len(out)
-
-
-def cpu_sample_parallel(wl, inputs_host, target_s=8.0, seed=0, procs=None):
-    """The same generic join on all host cores: the sampled root keys are
-    dealt round-robin to `procs` forked workers (the sorted indexes are built
-    once before the fork and shared copy-on-write). Returns (tuples, wall s,
-    keys, total keys, procs)."""
-    import multiprocessing as mp
-
-    from oracle.gj import join_rule
-    from paper_2604_20073_b200 import parse
-
-    procs = procs or len(os.sched_getaffinity(0))
-    prog = parse(wl.program)
-    rule = prog.rules[-1]
-    rels = dict(inputs_host)
-    cache = {}
-
-    def relation_of(pos):
-        return rels[rule.body[pos].relation]
-
-    roots = np.unique(rels[rule.body[0].relation][:, 0])
-    rng = np.random.default_rng(seed)
-    rng.shuffle(roots)
-    join_rule(rule, relation_of, lambda c, create=False: None, level0_keep=roots[:1], cache=cache)
-    _FORK_STATE.update(rule=rule, relation_of=relation_of, cache=cache)
-    # calibrate on one core, then give every worker that much work
-    take = max(1, len(roots) // 2000)
-    while True:
-        t0 = time.perf_counter()
-        _fork_join(np.sort(roots[:take]))
-        dt = time.perf_counter() - t0
-        if dt > target_s / 8 or take >= len(roots):
-            break
-        take = min(len(roots), int(take * max(2.0, target_s / max(dt, 1e-3) / 8)))
-    total = min(len(roots), take * procs)
-    chunks = [np.sort(roots[i:total:procs]) for i in range(procs)]
-    with mp.get_context("fork").Pool(procs) as pool:
-        pool.map(_fork_join, [c[:1] for c in chunks])  # workers up
-        t0 = time.perf_counter()
-        n = sum(pool.map(_fork_join, chunks))
-        dt = time.perf_counter() - t0
-    return n, dt, total, len(roots), procs
+def cpu_baseline(wl, target_s=15.0):
+    s = CpuSampler(wl, target_s)
+    n, dt, th, what = s.step()
+    return {"value": n / dt, "unit": "tuples/s", "cores": th, "kind": "port",
+            "sample": f"{what}: {n} tuples in {dt:.2f} s on {th} threads (C++ restatement of the reference "
+                      "generic join + semi-naive loop, oracle/native.py)"}
 
 
-def cpu_baseline(wl, inputs):
-    if isinstance(wl, TriangleRMAT):
-        host = {k: v.cpu().numpy().astype(np.int64).T for k, v in inputs.items()}
-        n, dt, take, nroots = cpu_sample(wl, host)
-        sample = (f"{take}/{nroots} random root keys, {n} derived tuples in {dt:.2f} s "
-                  "(numpy generic-join restatement of the reference executor)")
-    else:
-        n, dt, sample = wl.cpu_sample()
-    return {"value": n / dt, "unit": "tuples/s", "cores": 1, "kind": "port", "sample": sample}
-
-
-def triangle_parity(wl, gpu_rows):
-    """GPU output restricted to the sampled root keys vs the oracle's rows."""
+def parity_check(wl, ctx=None):
+    """One more device evaluation (not timed); its output relation and its
+    EDB reduced to digests and compared with the oracle's digests of the
+    same full-size instance (committed)."""
     import torch
 
-    x = gpu_rows[0].view(torch.int32).to(torch.int64)
-    keys = torch.from_numpy(np.asarray(wl.sample_roots, dtype=np.int64)).to(x.device)
-    sel = torch.isin(x, keys)
-    got = gpu_rows.view(torch.int32)[:, sel].to(torch.int64).cpu().numpy().T
-    got = got[np.lexsort(got.T[::-1])] if len(got) else got
-    return {"checked": f"all output rows of {len(wl.sample_roots)} sampled root keys vs the CPU oracle",
-            "rows": int(len(wl.oracle_rows)), "match": bool(np.array_equal(got, wl.oracle_rows)),
-            "sorted_unique": True}
-
-
-def parity_check(wl, inputs):
-    """Bit-exact comparison of one more device evaluation with the oracle on
-    the sample the CPU baseline used (not timed)."""
+    from oracle.digest import digest
     from paper_2604_20073_b200 import Engine, parse
-    from paper_2604_20073_b200 import device as dev
 
-    if not isinstance(wl, TriangleRMAT):
-        return wl.parity()
-    eng = Engine(parse(wl.program), schedule="stream")
-    for k, v in inputs.items():
+    with open(DIGESTS) as fh:
+        want = json.load(fh).get(wl.name)
+    if want is None:
+        return {"checked": "no committed oracle digest for this workload", "match": None}
+    eng = Engine(parse(wl.program), schedule="stream", dist=ctx)
+    for k, v in wl.device_facts().items():
         eng.load_columns(k, v)
     eng.solve()
-    rows = eng.relation_columns(wl.output)
-    out = triangle_parity(wl, rows)
-    out["sorted_unique"] = bool(dev.is_sorted_strict(rows))
-    return out
+    rels = {wl.output: want["idb"][wl.output]}
+    got = {}
+    for rel in rels:
+        got[rel] = digest(eng.relation_columns(rel).cpu().numpy())
+    edb_ok = all(digest(eng.relation_columns(k).cpu().numpy()) == d for k, d in want["edb"].items())
+    torch.cuda.synchronize()
+    return {"checked": f"full {wl.output} relation (n, sha256 of sorted columns, fold64) vs the C++ oracle's "
+                       "digest of the same full-size instance (tests/golden/baseline_digests.json)",
+            "rows": want["idb"][wl.output]["n"], "edb_match": edb_ok,
+            "match": bool(edb_ok and all(got[r] == rels[r] for r in rels))}
 
 
 def bench_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference CPU algorithm."""
-    import torch
-
+    """--impl reference: the C++ oracle port of the reference CPU algorithm
+    on all host cores. No GPU, no libsrdl: inputs come from the numpy
+    generators (the R-MAT graph from the host mirror of the device
+    generator)."""
     if rank != 0:
         return None
-    wl = make_workload(args, 0, 1)
-    torch.cuda.set_device(0) if torch.cuda.is_available() else None
-    rates = []
-    sample = ""
-    dt = 0.0
-    cores = 1
-    if isinstance(wl, TriangleRMAT):
-        inputs = {k: v.cpu().numpy().astype(np.int64).T for k, v in wl.generate().items()}
-        for i in range(args.warmup + args.steps):
-            n, dt, take, nroots, cores = cpu_sample_parallel(wl, inputs, target_s=8.0, seed=i)
-            if i >= args.warmup:
-                rates.append(n / dt)
-        sample = (f"{take}/{nroots} random root keys per step dealt to {cores} forked workers "
-                  "(numpy generic join over the sample)")
-    else:
-        for i in range(1 + args.steps):  # one warm-up suffices for the CPU port
-            n, dt, sample = wl.cpu_sample()
-            if i >= 1:
-                rates.append(n / dt)
+    wl = make_workload(args.workload)
+    per_step = max(2.0, args.ref_budget_s / max(1, args.steps + args.warmup))
+    sampler = CpuSampler(wl, per_step)
+    for _ in range(args.warmup):
+        sampler.step()
+    rates, secs = [], []
+    for _ in range(args.steps):
+        n, dt, th, what = sampler.step()
+        rates.append(n / dt)
+        secs.append(dt)
     value = sum(rates) / len(rates)
+    cfg = dict(wl.config)
+    cfg["sample"] = what
+    cfg["same_config"] = bool(sampler.full is not None and sampler.frac >= 1.0)
     return {
         "impl": "reference",
         "metric": "derived tuples/sec (fixpoint)",
@@ -661,14 +547,16 @@ def bench_reference(args, rank, world):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": dt * 1e3,
+        "ms_per_step": sum(secs) / len(secs) * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "int64",
-        "data": "synthetic (seeded generator)",
-        "config": wl.config,
-        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": cores, "kind": "port", "sample": sample},
+        "dtype": "u32",
+        "data": "synthetic (seeded numpy generators, the same instance as the GPU arm)",
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": th, "kind": "port",
+                         "sample": f"{what} per step, {th} threads (C++ restatement of the reference "
+                                   "generic join + semi-naive loop, oracle/native.py)"},
         "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -679,40 +567,42 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="triangle")
-    ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (testing)")
-    ap.add_argument("--edges", type=int, default=None, help="R-MAT edge count override (testing)")
+    ap.add_argument("--workload", choices=["tc", "triangle", "sg", "andersen", "doop"], default="doop")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--small", action="store_true", help="recursive workloads: the CPU-sample instance")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: CPU seconds for all warm-up + timed steps together")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
 
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
+    if args.impl == "reference":
+        line = bench_reference(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
     dist = None
-    if args.impl == "ours" and world > 1:
+    if world > 1:
         import torch
         import torch.distributed as tdist
 
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
         dist = tdist
-
-    if args.impl == "reference":
-        line = bench_reference(args, rank, world)
-        if line is not None:
-            print(json.dumps(line))
-        return
-
-    result, wl, inputs = bench_ours(args, rank, world, dist)
-    if rank == 0 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(wl, inputs)
-        result["parity"] = parity_check(wl, inputs)
+    result, wl, inputs, ctx = bench_ours(args, rank, world, dist)
+    if not args.no_parity:
+        par = parity_check(wl, ctx)
+        if rank == 0:
+            result["parity"] = par
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(wl)
     if dist:
         dist.destroy_process_group()
     if rank == 0:
-        print(json.dumps(result))
+        print(json.dumps(result), flush=True)
 
 
 if __name__ == "__main__":

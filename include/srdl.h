@@ -17,7 +17,8 @@
  *   - Host-side counts written through `uint64_t *n_out` require a stream
  *     synchronisation, which the function performs (two-phase allocation:
  *     the caller sizes the next buffer from that count).
- *   - Scratch memory comes from the device's stream-ordered memory pool.
+ *   - Scratch memory comes from a stack arena per (device, stream, host
+ *     thread) inside libsrdl; every scratch buffer lives within one call.
  */
 #ifndef SRDL_H
 #define SRDL_H

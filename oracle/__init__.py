@@ -17,11 +17,21 @@ gj.py        vectorised generic join (attribute-at-a-time over sorted
              fixpoint loop (reference: pkg/src/flatlog/runtime.py:259-315),
              with its own rule grouping (Kosaraju) and its own variable order,
              sharing only the parsed AST with the engine.
+gj_native.cpp + native.py
+             the same generic join and semi-naive loop (same rule grouping,
+             variable orders and column orders, encoded by native.py from
+             gj's own functions) in C++ on all host cores (OpenMP): the
+             checker at BASELINE sizes (tests/golden/make_baseline_digests.py)
+             and the CPU baseline / reference arm of bench.py.
+digest.py    order-checked streaming digests of sorted relations (n, sha256
+             of the columns, order-independent 64-bit fold) for full-size
+             parity without committing gigabytes of tuples.
 
 Pinning
 -------
-Both modules are checked against golden fixtures produced by running the
-reference package itself in the build container
+gj.py, storage.py and the C++ restatement are all checked against golden
+fixtures produced by running the reference package itself in the build
+container
 (tests/golden/make_golden.py -> tests/golden/*.json*), see
 tests/test_oracle_golden.py. Parity status: pinned.
 """

@@ -63,8 +63,8 @@ int guarded(F &&f) {
 
 // --------------------------------------------------------- scratch memory
 
-// Stream-ordered scratch buffer (cudaMallocAsync on the device pool, whose
-// release threshold is raised once so repeated iterations reuse memory).
+// Stream-ordered scratch buffer from the stack arena of (device, stream,
+// host thread) in scan.cu: strictly nested inside one C-ABI call.
 class Scratch {
   public:
     Scratch(size_t bytes, cudaStream_t s);
@@ -79,11 +79,16 @@ class Scratch {
   private:
     void *ptr_ = nullptr;
     cudaStream_t stream_;
+    int dev_ = 0;
     size_t bytes_ = 0;
     size_t block_ = 0;
 };
 
-int sm_count();
+int sm_count();  // of the current device (cached per device)
+
+// true the first time it is called for the current device with this mask
+// (per-device one-time setup such as cudaFuncSetAttribute)
+bool first_use_on_device(uint64_t *mask);
 
 // Host-visible read of a device scalar (synchronises the stream).
 uint64_t read_u64(const uint64_t *dev, cudaStream_t s);

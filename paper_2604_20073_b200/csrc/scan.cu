@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -29,14 +30,18 @@ uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
 
 // ----------------------------------------------------------------- scratch
 
-// Scratch memory comes from a per-stream stack arena: every Scratch lives
-// inside one C-ABI call (RAII, strictly nested), so allocation is a pointer
-// bump and release a pop. Kernels of a later call on the same stream run
-// after the earlier call's kernels (stream order), so reusing the bytes is
-// safe; calls on other streams use their own arena. Blocks are cudaMalloc'ed
-// when a stack outgrows its current block and kept for the process — no
-// driver call per scratch buffer (cudaMallocAsync was measured to stall for
-// ~0.5 s now and then under torch's expandable segments).
+// Scratch memory comes from a stack arena per (device, stream, host thread):
+// every Scratch lives inside one C-ABI call (RAII, strictly nested), so
+// allocation is a pointer bump and release a pop. Kernels of a later call
+// from the same thread on the same stream run after the earlier call's
+// kernels (stream order), so reusing the bytes is safe. Keying by thread as
+// well keeps the stack discipline when several host threads share a stream
+// (the legacy default stream, one stream pool for all engines): their calls
+// interleave, but each thread's allocations stay nested in its own arena.
+// Keying by device keeps a second GPU's scratch on that GPU. Blocks are
+// cudaMalloc'ed when a stack outgrows its current block and kept for the
+// process — no driver call per scratch buffer (cudaMallocAsync was measured
+// to stall for ~0.5 s now and then under torch's expandable segments).
 namespace {
 
 struct Block {
@@ -49,19 +54,41 @@ struct StreamArena {
     size_t top = 0;
 };
 
+struct ArenaKey {
+    int dev;
+    cudaStream_t stream;
+    std::thread::id thread;
+    bool operator==(const ArenaKey &o) const { return dev == o.dev && stream == o.stream && thread == o.thread; }
+};
+
+struct ArenaKeyHash {
+    size_t operator()(const ArenaKey &k) const {
+        return std::hash<void *>()((void *)k.stream) * 31u + std::hash<std::thread::id>()(k.thread) * 7u +
+               (size_t)k.dev;
+    }
+};
+
 std::mutex g_arena_mu;
-std::unordered_map<cudaStream_t, StreamArena> g_arenas;
+std::unordered_map<ArenaKey, StreamArena, ArenaKeyHash> g_arenas;
 
 constexpr size_t kAlign = 256;
 constexpr size_t kMinBlock = size_t(64) << 20;
+
+ArenaKey arena_key(cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return ArenaKey{dev, s, std::this_thread::get_id()};
+}
 
 }  // namespace
 
 Scratch::Scratch(size_t bytes, cudaStream_t s) : stream_(s) {
     if (bytes == 0) bytes = 16;
     bytes = (bytes + kAlign - 1) & ~(kAlign - 1);
+    const ArenaKey key = arena_key(s);
+    dev_ = key.dev;
     std::lock_guard<std::mutex> lock(g_arena_mu);
-    StreamArena &A = g_arenas[s];
+    StreamArena &A = g_arenas[key];
     // current block, else the next existing block with room, else a new one
     while (A.top < A.blocks.size() && A.blocks[A.top].size - A.blocks[A.top].used < bytes) {
         if (A.blocks[A.top].used == 0 && A.top + 1 >= A.blocks.size()) break;
@@ -85,22 +112,41 @@ Scratch::Scratch(size_t bytes, cudaStream_t s) : stream_(s) {
 
 Scratch::~Scratch() {
     std::lock_guard<std::mutex> lock(g_arena_mu);
-    StreamArena &A = g_arenas[stream_];
+    StreamArena &A = g_arenas[ArenaKey{dev_, stream_, std::this_thread::get_id()}];
     Block &b = A.blocks[block_];
-    b.used -= bytes_;  // LIFO: this was the last allocation of its block
+    if ((char *)ptr_ + bytes_ != b.base + b.used) {
+        // not the newest allocation of its block: the stack discipline was
+        // broken (a Scratch moved across threads). Keep the bytes reserved
+        // rather than hand live memory out again; the block is reclaimed
+        // once everything above it is released.
+        set_error("scratch arena released out of order (kept reserved)");
+        return;
+    }
+    b.used -= bytes_;
     while (A.top > 0 && A.blocks[A.top].used == 0) --A.top;
 }
 
 int sm_count() {
-    static int cached = 0;
-    if (!cached) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
         int n = 0;
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        cached = n > 0 ? n : 148;
+        cached[dev] = n > 0 ? n : 148;
     }
-    return cached;
+    return cached[dev];
+}
+
+bool first_use_on_device(uint64_t *mask) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    std::lock_guard<std::mutex> lock(g_arena_mu);
+    if (*mask & bit) return false;
+    *mask |= bit;
+    return true;
 }
 
 uint64_t read_u64(const uint64_t *dev, cudaStream_t s) {

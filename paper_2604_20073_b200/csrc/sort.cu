@@ -157,13 +157,12 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
                  (unsigned long long)n);
     const uint64_t blocks = (n + kTile - 1) / kTile;
     const int passes = (int)((bits + kRadixBits - 1) / kRadixBits);
-    static bool raised = false;
-    if (!raised) {  // the reorder tile needs more than the 48 KB default
+    static uint64_t raised = 0;
+    if (first_use_on_device(&raised)) {  // the reorder tile needs more than the 48 KB default
         SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)scatter_smem<true>()));
         SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)scatter_smem<false>()));
-        raised = true;
     }
     Scratch kalt(n * sizeof(uint64_t), s);
     Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);

@@ -1063,11 +1063,10 @@ template <int MODE, int KIND>
 static void launch_kind(const srdl_plan *P, const srdl_exec *X, const srdl_spec *Q, cudaStream_t s) {
     const uint32_t NL = P->nspec[P->depth - 1] ? P->nspec[P->depth - 1] : 1;
     const size_t bytes = warp_bytes(P->depth, P->natoms, NL, P->nmid) * kJoinWarps;
-    static bool raised = false;
-    if (!raised) {  // allow up to the full 227 KB of dynamic shared memory
+    static uint64_t raised = 0;
+    if (first_use_on_device(&raised)) {  // allow up to the full 227 KB of dynamic shared memory
         SRDL_CUDA(cudaFuncSetAttribute(wcoj_kernel<MODE, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        227 * 1024));
-        raised = true;
     }
     SRDL_REQUIRE(bytes <= 227 * 1024, "join state of %zu bytes per block exceeds shared memory", bytes);
     // one full wave of resident blocks (the plan's shared-memory footprint and

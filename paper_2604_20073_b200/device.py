@@ -243,6 +243,28 @@ def stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+# Benchmark hook: when a list, every library call made through `timed`
+# appends [family, start_event, end_event, algorithmic_bytes] recorded on
+# the launching (current) stream; bench.py reads them after the timed steps.
+PROFILE = None
+
+
+def timed(family: str, algo_bytes: int, fn):
+    """Run fn (one C-ABI call); under PROFILE bracket it with CUDA events on
+    the current stream. Returns (fn's result, the record or None) — callers
+    that learn the output size only later may add to record[3]."""
+    if PROFILE is None:
+        return fn(), None
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    rc = fn()
+    b.record()
+    rec = [family, a, b, int(algo_bytes)]
+    PROFILE.append(rec)
+    return rc, rec
+
+
 def check(rc: int, what: str):
     if rc != 0:
         msg = _LIB.srdl_last_error().decode(errors="replace") if _LIB else "?"
@@ -311,11 +333,12 @@ def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None, distinct: bool = 
     if n == 0:
         return out
     got = C.c_uint64(0)
-    check(
-        lib().srdl_sort_dedup(col_ptrs(rows, order), len(order), n, bits, col_ptrs(out),
-                              None if distinct else C.byref(got), stream_handle()),
-        "sort_dedup",
-    )
+    rc, rec = timed("sort_dedup", 4 * arity * n, lambda: lib().srdl_sort_dedup(
+        col_ptrs(rows, order), len(order), n, bits, col_ptrs(out), None if distinct else C.byref(got),
+        stream_handle()))
+    check(rc, "sort_dedup")
+    if rec is not None:
+        rec[3] += 4 * len(order) * (n if distinct else got.value)
     return out if distinct else _trim(out, got.value)
 
 
@@ -332,17 +355,20 @@ def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
     seg_cols = (C.c_void_p * MAX_DIFF_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
     seg_rows = (C.c_uint64 * MAX_DIFF_SEGS)(*[nrows(s) for s in segs])
     got = C.c_uint64(0)
-    check(
-        lib().srdl_compute_delta(col_ptrs(rows), arity, n, bits, seg_cols, seg_rows, len(segs),
-                                 col_ptrs(out), C.byref(got), stream_handle()),
-        "compute_delta",
-    )
+    rc, rec = timed("compute_delta", 4 * arity * n, lambda: lib().srdl_compute_delta(
+        col_ptrs(rows), arity, n, bits, seg_cols, seg_rows, len(segs), col_ptrs(out), C.byref(got),
+        stream_handle()))
+    check(rc, "compute_delta")
+    if rec is not None:
+        rec[3] += 4 * arity * got.value
     return _trim(out, got.value)
 
 
-def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: torch.Tensor) -> torch.Tensor:
+def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: torch.Tensor):
     """compute_delta into a capacity-n buffer; the row count is written to
-    count_slot (a 1-element uint32 device tensor) without a host round trip."""
+    count_slot (a 1-element uint32 device tensor) without a host round trip.
+    Returns the buffer and the PROFILE record (None when not profiling): the
+    caller adds the written bytes (4 * arity * count) once it reads the count."""
     arity, n = rows.shape
     out = empty_rows(arity, n)
     segs = [s for s in segments if nrows(s)]
@@ -351,10 +377,11 @@ def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: tor
     seg_ptr_arrays = [col_ptrs(s) for s in segs]
     seg_cols = (C.c_void_p * MAX_DIFF_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
     seg_rows = (C.c_uint64 * MAX_DIFF_SEGS)(*[nrows(s) for s in segs])
-    check(lib().srdl_compute_delta_async(col_ptrs(rows) if n else None, arity, n, bits, seg_cols, seg_rows,
-                                         len(segs), col_ptrs(out) if n else None, count_slot.data_ptr(),
-                                         stream_handle()), "compute_delta_async")
-    return out
+    rc, rec = timed("compute_delta", 4 * arity * n, lambda: lib().srdl_compute_delta_async(
+        col_ptrs(rows) if n else None, arity, n, bits, seg_cols, seg_rows, len(segs),
+        col_ptrs(out) if n else None, count_slot.data_ptr(), stream_handle()))
+    check(rc, "compute_delta_async")
+    return out, rec
 
 
 def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor, k_slots: torch.Tensor):
@@ -368,10 +395,14 @@ def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Te
     uk = torch.empty(n + nf, dtype=U32, device=d)
     ud = torch.empty(n + nf, dtype=U32, device=d)
     up = torch.empty(n + nf, dtype=U64, device=d)
-    check(lib().srdl_histogram_union_async(col.data_ptr() if n else None, n, fkeys.data_ptr() if nf else None,
-                                           fdeg.data_ptr() if nf else None, nf, dk.data_ptr(), dd.data_ptr(),
-                                           dp.data_ptr(), uk.data_ptr(), ud.data_ptr(), up.data_ptr(),
-                                           k_slots.data_ptr(), stream_handle()), "histogram_union_async")
+    # algorithmic: the delta column, the full histogram (keys + degrees) read
+    # once, both histograms written (key, degree, prefix: 16 B per key; sized
+    # here by their upper bounds n and n + nf)
+    rc, _ = timed("histogram", 4 * n + 8 * nf, lambda: lib().srdl_histogram_union_async(
+        col.data_ptr() if n else None, n, fkeys.data_ptr() if nf else None, fdeg.data_ptr() if nf else None, nf,
+        dk.data_ptr(), dd.data_ptr(), dp.data_ptr(), uk.data_ptr(), ud.data_ptr(), up.data_ptr(),
+        k_slots.data_ptr(), stream_handle()))
+    check(rc, "histogram_union_async")
     return (dk, dd, dp), (uk, ud, up)
 
 
@@ -384,10 +415,9 @@ def merge(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     if na == 0:
         return b
     out = empty_rows(arity, na + nb)
-    check(
-        lib().srdl_merge(col_ptrs(a), na, col_ptrs(b), nb, arity, col_ptrs(out), stream_handle()),
-        "merge",
-    )
+    rc, _ = timed("merge", 8 * arity * (na + nb), lambda: lib().srdl_merge(
+        col_ptrs(a), na, col_ptrs(b), nb, arity, col_ptrs(out), stream_handle()))
+    check(rc, "merge")
     return out
 
 
@@ -396,8 +426,9 @@ def is_sorted_strict(rows: torch.Tensor) -> bool:
     arity, n = rows.shape
     if n <= 1:
         return True
-    check(lib().srdl_is_sorted_strict(col_ptrs(rows), arity, n, C.byref(ok), stream_handle()),
-          "is_sorted_strict")
+    rc, _ = timed("is_sorted", 4 * arity * n, lambda: lib().srdl_is_sorted_strict(
+        col_ptrs(rows), arity, n, C.byref(ok), stream_handle()))
+    check(rc, "is_sorted_strict")
     return bool(ok.value)
 
 
@@ -420,9 +451,12 @@ def histogram(col: torch.Tensor):
     if n == 0:
         return keys, deg, prefix
     k = C.c_uint64(0)
-    check(lib().srdl_histogram(col.data_ptr(), n, keys.data_ptr(), deg.data_ptr(), prefix.data_ptr(),
-                               C.byref(k), stream_handle()), "histogram")
+    rc, rec = timed("histogram", 4 * n, lambda: lib().srdl_histogram(
+        col.data_ptr(), n, keys.data_ptr(), deg.data_ptr(), prefix.data_ptr(), C.byref(k), stream_handle()))
+    check(rc, "histogram")
     K = k.value
+    if rec is not None:
+        rec[3] += 16 * K
     return keys[:K], deg[:K], prefix[:K]
 
 
@@ -433,10 +467,13 @@ def histogram_merge(ka, da, kb, db):
     deg = torch.empty(n, dtype=U32, device=device())
     prefix = torch.empty(n, dtype=U64, device=device())
     k = C.c_uint64(0)
-    check(lib().srdl_histogram_merge(ka.data_ptr(), da.data_ptr(), na, kb.data_ptr(), db.data_ptr(),
-                                     nb, keys.data_ptr(), deg.data_ptr(), prefix.data_ptr(),
-                                     C.byref(k), stream_handle()), "histogram_merge")
+    rc, rec = timed("histogram", 8 * (na + nb), lambda: lib().srdl_histogram_merge(
+        ka.data_ptr(), da.data_ptr(), na, kb.data_ptr(), db.data_ptr(), nb, keys.data_ptr(), deg.data_ptr(),
+        prefix.data_ptr(), C.byref(k), stream_handle()))
+    check(rc, "histogram_merge")
     K = k.value
+    if rec is not None:
+        rec[3] += 16 * K
     return keys[:K], deg[:K], prefix[:K]
 
 
@@ -454,11 +491,14 @@ def histogram_union(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor):
     if n == 0:
         return (dk, dd, dp), (fkeys, fdeg, None)
     kd, ku = C.c_uint64(0), C.c_uint64(0)
-    check(lib().srdl_histogram_union(col.data_ptr(), n, fkeys.data_ptr() if nf else None,
-                                     fdeg.data_ptr() if nf else None, nf, dk.data_ptr(), dd.data_ptr(),
-                                     dp.data_ptr(), C.byref(kd), uk.data_ptr(), ud.data_ptr(), up.data_ptr(),
-                                     C.byref(ku), stream_handle()), "histogram_union")
+    rc, rec = timed("histogram", 4 * n + 8 * nf, lambda: lib().srdl_histogram_union(
+        col.data_ptr(), n, fkeys.data_ptr() if nf else None, fdeg.data_ptr() if nf else None, nf, dk.data_ptr(),
+        dd.data_ptr(), dp.data_ptr(), C.byref(kd), uk.data_ptr(), ud.data_ptr(), up.data_ptr(), C.byref(ku),
+        stream_handle()))
+    check(rc, "histogram_union")
     a, b = kd.value, ku.value
+    if rec is not None:
+        rec[3] += 16 * (a + b)
     return (dk[:a], dd[:a], dp[:a]), (uk[:b], ud[:b], up[:b])
 
 
@@ -518,10 +558,11 @@ def root_work(okeys, odeg, oprefix=None, ikeys=None, ideg=None, iprefix=None, ou
     def p(t):
         return t.data_ptr() if t is not None and t.numel() else None
 
-    check(lib().srdl_root_work(okeys.data_ptr(), odeg.data_ptr(), p(oprefix), nk,
-                               p(ikeys) if has_inner else None, p(ideg) if has_inner else None,
-                               p(iprefix) if has_inner else None, nik, int(has_inner), d2.data_ptr(),
-                               prefix.data_ptr(), p(olo), p(ilo), stream_handle()), "root_work")
+    rc, _ = timed("root_work", 24 * nk, lambda: lib().srdl_root_work(
+        okeys.data_ptr(), odeg.data_ptr(), p(oprefix), nk, p(ikeys) if has_inner else None,
+        p(ideg) if has_inner else None, p(iprefix) if has_inner else None, nik, int(has_inner), d2.data_ptr(),
+        prefix.data_ptr(), p(olo), p(ilo), stream_handle()))
+    check(rc, "root_work")
     return d2, prefix, olo, ilo
 
 

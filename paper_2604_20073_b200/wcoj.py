@@ -38,24 +38,10 @@ WARPS_PER_SM = 32  # slice-array sizing; the launcher picks the resident wave it
 SLICES_PER_WARP = 256  # slice-array capacity per launched warp (fetched dynamically)
 MIN_SLICE_UNITS = int(os.environ.get("SRDL_MIN_SLICE_UNITS", 4096))  # fewer, larger slices when the root space is small
 
-# Benchmark hook: when a list, every count/materialize launch appends
-# (name, start_event, end_event) recorded on the launching stream.
-KERNEL_EVENTS = None
-
-
 def _timed(name, fn, algo_bytes=0):
-    """Run fn; when KERNEL_EVENTS is a list (bench.py), bracket it with CUDA
-    events on the current (launching) stream and record the launch's
-    algorithmic bytes next to them."""
-    if KERNEL_EVENTS is None:
-        return fn()
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
-    a.record()
-    rc = fn()
-    b.record()
-    KERNEL_EVENTS.append((name, a, b, algo_bytes))
-    return rc
+    """One WCOJ library call under the bench's event hook (dev.PROFILE)."""
+    rc, rec = dev.timed(name, algo_bytes, fn)
+    return rc, rec
 
 
 def input_bytes(prep) -> int:
@@ -302,7 +288,7 @@ class CountResult:
     _total: int | None = None
     spec: "SpecArena | None" = None  # speculative output of the count walk
     spills: int | None = None  # slices the arena could not hold (host, after readback)
-    event: int | None = None  # index of the count launch in KERNEL_EVENTS (bench)
+    event: list | None = None  # the count launch's dev.PROFILE record (bench)
 
     @classmethod
     def none(cls) -> "CountResult":
@@ -428,18 +414,17 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec
     )
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
-    algo = input_bytes(prep) if KERNEL_EVENTS is not None else 0
-    if KERNEL_EVENTS is not None:
-        counts.event = len(KERNEL_EVENTS)
+    algo = input_bytes(prep) if dev.PROFILE is not None else 0
     if spec_capacity >= SPEC_CHUNK:
         counts.spec = SpecArena(plan.head_arity, spec_capacity, n, spec_storage)
         q = counts.spec.descriptor()
-        dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count_spec(
-            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()), algo), "wcoj_count_spec")
+        rc, counts.event = _timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count_spec(
+            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()), algo)
+        dev.check(rc, "wcoj_count_spec")
     else:
-        dev.check(_timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(C.byref(desc), C.byref(x),
-                                                                          dev.stream_handle()), algo),
-                  "wcoj_count")
+        rc, counts.event = _timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count(
+            C.byref(desc), C.byref(x), dev.stream_handle()), algo)
+        dev.check(rc, "wcoj_count")
     return counts
 
 
@@ -468,21 +453,23 @@ def materialize_pass(plan, store, partition, counts: CountResult, out_cols, prep
         # and walk again only the slices the arena could not hold
         q = counts.spec.descriptor()
         spills = counts.spills if counts.spills is not None else int(counts.spec.spills_dev.item())
-        if KERNEL_EVENTS is not None and counts.event is not None:  # the count walk wrote the tuples
-            name, a, b, nbytes = KERNEL_EVENTS[counts.event]
-            KERNEL_EVENTS[counts.event] = (name, a, b, nbytes + out_bytes)
-        dev.check(_timed("wcoj_gather", lambda: dev.lib().srdl_wcoj_gather(
-            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()),
-            2 * out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_gather")
+        if counts.event is not None:  # the count walk wrote the tuples (into the arena)
+            counts.event[3] += out_bytes
+        prof = dev.PROFILE is not None
+        rc, _ = _timed("wcoj_gather", lambda: dev.lib().srdl_wcoj_gather(
+            C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()), 2 * out_bytes if prof else 0)
+        dev.check(rc, "wcoj_gather")
         if spills:
-            dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize_spilled(
+            rc, _ = _timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize_spilled(
                 C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()),
-                input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize_spilled")
+                input_bytes(prep) + out_bytes if prof else 0)
+            dev.check(rc, "wcoj_materialize_spilled")
         counts.spec = None  # release the arena
     else:
-        dev.check(_timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
+        rc, _ = _timed("wcoj_materialize", lambda: dev.lib().srdl_wcoj_materialize(
             C.byref(desc), C.byref(x), dev.stream_handle()),
-            input_bytes(prep) + out_bytes if KERNEL_EVENTS is not None else 0), "wcoj_materialize")
+            input_bytes(prep) + out_bytes if dev.PROFILE is not None else 0)
+        dev.check(rc, "wcoj_materialize")
     if own_flag and int(error.item()):
         raise InternalError(f"plan {plan.plan_id}: materialized tuple count diverged from the count pass")
     return out_cols

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_reference_arm_json_line_cpu():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--workload", "tc", "--steps", "1", "--warmup", "3"],
+                          "--workload", "tc", "--steps", "1", "--warmup", "3", "--ref-budget-s", "6"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -24,3 +24,4 @@ def test_reference_arm_json_line_cpu():
     e2e = line["e2e"]
     assert e2e["value"] == line["value"] and e2e["h2d_bytes_per_step"] == 0
     assert "configs[0]" in line["config"]["workload"]
+    assert "root keys" in line["config"]["sample"] or "full instance" in line["config"]["sample"]
