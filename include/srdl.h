@@ -23,7 +23,18 @@
 #ifndef SRDL_H
 #define SRDL_H
 
+#ifdef __CUDACC_RTC__
+/* NVRTC (the per-plan kernel JIT, csrc/wcoj_jit.cu) has no C library
+ * headers; the fixed-width types come from here. */
+typedef unsigned char uint8_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned long size_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -281,6 +292,35 @@ int srdl_wcoj_gather(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec
 /* srdl_wcoj_materialize restricted to the slices flagged in spec->slice_spill. */
 int srdl_wcoj_materialize_spilled(const srdl_plan *plan, const srdl_exec *ex, const srdl_spec *spec,
                                   void *stream);
+
+/* ---------------------------------------------------- per-rule kernels
+ * The compiler half of the paper (rules become CUDA kernels, PAPER.md:231;
+ * no reference counterpart: the reference interprets plans in numpy,
+ * executor.py:342-431). For the static shape of a plan (the srdl_plan
+ * fields other than pointers, row ranges and segment counts) the library
+ * generates and NVRTC-compiles a kernel with that shape as compile-time
+ * constants (csrc/wcoj_jit.cu), cached per shape in process and on disk
+ * ($SRDL_JIT_CACHE, default ~/.cache/srdl-jit). srdl_wcoj_count /
+ * _count_spec / _materialize* use it when it is built and fall back to the
+ * generic kernel of the plan's class otherwise; both give identical
+ * results. Mode: SRDL_JIT=0 (off) | async (default) | sync. */
+
+/* Schedule the kernels of n plans (array of descriptors; only the shape
+ * fields are read) in `mode` (0 count, 1 materialize, 2 speculative count)
+ * on the background compiler; wait != 0 blocks until they are built.
+ * Returns how many of them have a kernel ready. */
+int srdl_wcoj_jit_prepare(const srdl_plan *plans, uint32_t n, int mode, int wait);
+/* Block until the background compiler is idle. */
+void srdl_wcoj_jit_wait(void);
+/* 0 off, 1 async, 2 sync; returns the previous mode. */
+int srdl_wcoj_jit_set_mode(int mode);
+/* Generated source of a plan's kernel (truncated to cap bytes); returns its length. */
+uint64_t srdl_wcoj_jit_source(const srdl_plan *plan, int mode, char *buf, uint64_t cap);
+/* NVRTC-compile without loading (no GPU needed): 0 ok (*cubin_bytes set),
+ * 1 compile error (log in srdl_last_error), 2 NVRTC unavailable. */
+int srdl_wcoj_jit_compile_check(const srdl_plan *plan, int mode, uint64_t *cubin_bytes);
+/* out[4] = kernels compiled, disk-cache hits, failures, mode in effect. */
+void srdl_wcoj_jit_stats(uint64_t *out);
 
 /* ------------------------------------------------------------ multi-GPU
  * Owner of a value among `world` ranks (hash partitioning of root keys):

@@ -18,8 +18,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsrdl.so")
-SOURCES = ["scan.cu", "sort.cu", "setops.cu", "wcoj.cu"]
+SOURCES = ["scan.cu", "sort.cu", "setops.cu", "wcoj.cu", "wcoj_mode0.cu", "wcoj_mode1.cu", "wcoj_mode2.cu",
+           "wcoj_jit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+LIBS = ["-ldl"]  # NVRTC is opened with dlopen (csrc/wcoj_jit.cu)
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
@@ -37,28 +39,47 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(f) <= built for f in _inputs())
 
 
+def _compile_and_link(out: str, defines=(), verbose=False) -> str:
+    """Each source compiled on its own thread (the WCOJ instances dominate),
+    then one link into `out`."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    objdir = os.path.join(HERE, "build", os.path.basename(out))
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+
+    def one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [nvcc, *ARCH, *FLAGS, *dflags, "-I", INCLUDE, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        objs = list(pool.map(one, SOURCES))
+    tmp = out + ".tmp"
+    cmd = [nvcc, *ARCH, *FLAGS, "-o", tmp, *objs, *LIBS]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
+    os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    tmp = LIB + ".tmp"
-    cmd = [nvcc, *ARCH, *FLAGS, "-I", INCLUDE, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    return _compile_and_link(LIB, verbose=verbose)
 
 
 def build_variant(name: str, defines: list) -> str:
     """libsrdl_<name>.so with extra -D flags, for A/B runs selected through
     SRDL_LIBRARY (never loaded unless asked for)."""
-    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    out = os.path.join(HERE, f"libsrdl_{name}.so")
-    cmd = [nvcc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-o", out,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
-    subprocess.run(cmd, check=True)
-    return out
+    return _compile_and_link(os.path.join(HERE, f"libsrdl_{name}.so"), defines)
 
 
 if __name__ == "__main__":

@@ -161,17 +161,40 @@ __global__ void narrow_prefix_kernel(Cols cols, uint64_t n, const uint32_t *__re
     range[1] = hi;
 }
 
+// CSR offsets of a sorted key list over the id space [0, n_ids]: off[v] =
+// rows with key < v. Each thread owns kIdsPerThread consecutive ids, finds
+// the first key >= its first id by one binary search and walks forward, so
+// the work is O(n_ids + nk) plus one search per tile (instead of one search
+// per id); consecutive threads write consecutive 64-byte runs.
+constexpr uint32_t kIdsPerThread = 16;
+
 __global__ void dense_offsets_kernel(const uint32_t *__restrict__ keys,
                                      const uint64_t *__restrict__ prefix, uint64_t nk,
                                      uint32_t n_ids, uint32_t *__restrict__ off) {
-    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= n_ids;
-         v += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t lo = 0, hi = nk;  // first key >= v
+    const uint64_t ntiles = ((uint64_t)n_ids + kIdsPerThread) / kIdsPerThread;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v0 = t * kIdsPerThread;
+        uint64_t lo = 0, hi = nk;  // first key >= v0
         while (lo < hi) {
-            uint64_t m = (lo + hi) >> 1;
-            if (keys[m] < v) lo = m + 1; else hi = m;
+            const uint64_t m = (lo + hi) >> 1;
+            if (__ldg(keys + m) < v0) lo = m + 1; else hi = m;
         }
-        off[v] = lo ? (uint32_t)prefix[lo - 1] : 0u;
+        uint32_t vals[kIdsPerThread];
+#pragma unroll
+        for (uint32_t j = 0; j < kIdsPerThread; ++j) {
+            const uint64_t v = v0 + j;
+            while (lo < nk && __ldg(keys + lo) < v) ++lo;
+            vals[j] = lo ? (uint32_t)__ldg(prefix + lo - 1) : 0u;
+        }
+        if (v0 + kIdsPerThread <= (uint64_t)n_ids + 1) {
+            uint4 *dst = reinterpret_cast<uint4 *>(off + v0);  // off is 16-byte aligned (allocator)
+#pragma unroll
+            for (uint32_t j = 0; j < kIdsPerThread / 4; ++j)
+                dst[j] = make_uint4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+        } else {
+            for (uint32_t j = 0; v0 + j <= (uint64_t)n_ids; ++j) off[v0 + j] = vals[j];
+        }
     }
 }
 
@@ -519,8 +542,9 @@ int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nk
                        uint32_t n_ids, uint32_t *off, void *stream) {
     return guarded([&] {
         cudaStream_t s = (cudaStream_t)stream;
-        dense_offsets_kernel<<<stride_grid((uint64_t)n_ids + 1), kThreads, 0, s>>>(keys, prefix, nkeys,
-                                                                                  n_ids, off);
+        SRDL_REQUIRE(((uintptr_t)off & 15) == 0, "dense offsets buffer must be 16-byte aligned");
+        dense_offsets_kernel<<<stride_grid(((uint64_t)n_ids + kIdsPerThread) / kIdsPerThread), kThreads, 0, s>>>(
+            keys, prefix, nkeys, n_ids, off);
         SRDL_CHECK_LAUNCH();
     });
 }

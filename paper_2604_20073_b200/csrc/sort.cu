@@ -358,13 +358,20 @@ __global__ void gather_cols(Cols cols, uint32_t arity, const uint32_t *__restric
     }
 }
 
-// bad = 1 if some row is greater than (strict: not less than) its successor
+// bad = 1 if some row is greater than (strict: not less than) its successor.
+// Unsorted input is the common case (staged join output): one atomic per
+// warp that sees an inversion, and every warp stops once the flag is set
+// (a per-thread atomic on the same word serialised millions of them).
 __global__ void check_sorted(Cols rows, uint64_t n, uint32_t arity, int strict, int *bad) {
     const int limit = strict ? 0 : 1;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i + 1 < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if (row_cmp(rows, i, rows, i + 1, arity) >= limit) {
-            atomicExch(bad, 1);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x; base + 1 < n; base += stride) {
+        if (*(volatile int *)bad) return;  // warp-uniform
+        const uint64_t i = base + threadIdx.x;
+        const bool inv = i + 1 < n && row_cmp(rows, i, rows, i + 1, arity) >= limit;
+        const uint32_t m = __ballot_sync(0xffffffffu, inv);
+        if (m) {
+            if (lane_id() == 0) atomicExch(bad, 1);
             return;
         }
     }

@@ -1,0 +1,7 @@
+// WCOJ kernel instances of mode kCount (one translation unit per mode so
+// the build compiles the instances in parallel).
+#include "wcoj_launch.cuh"
+
+namespace srdl {
+template void launch<kCount>(const srdl_plan *, const srdl_exec *, const srdl_spec *, cudaStream_t);
+}  // namespace srdl

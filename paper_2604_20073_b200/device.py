@@ -184,6 +184,12 @@ _SIGNATURES = {
          C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
     "srdl_wcoj_count": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
+    "srdl_wcoj_jit_prepare": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int, C.c_int]),
+    "srdl_wcoj_jit_wait": (None, []),
+    "srdl_wcoj_jit_set_mode": (C.c_int, [C.c_int]),
+    "srdl_wcoj_jit_source": (C.c_uint64, [C.c_void_p, C.c_int, C.c_char_p, C.c_uint64]),
+    "srdl_wcoj_jit_compile_check": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
+    "srdl_wcoj_jit_stats": (None, [C.POINTER(C.c_uint64)]),
     "srdl_wcoj_materialize": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
     "srdl_route_rows": (
         C.c_int,
@@ -233,6 +239,29 @@ def lib():
         if _LIB.srdl_version() != 1:
             raise DeviceUnavailable("libsrdl.so version mismatch; rebuild it")
     return _LIB
+
+
+JIT_MODES = {"off": 0, "async": 1, "sync": 2}
+
+
+def jit_stats() -> dict:
+    """Per-plan kernel compiler counters (csrc/wcoj_jit.cu)."""
+    out = (C.c_uint64 * 4)()
+    lib().srdl_wcoj_jit_stats(out)
+    mode = {v: k for k, v in JIT_MODES.items()}.get(int(out[3]), "?")
+    return {"compiled": int(out[0]), "disk_hits": int(out[1]), "failures": int(out[2]), "mode": mode}
+
+
+def jit_mode(mode: str) -> str:
+    """Set the per-plan kernel mode ("off", "async", "sync"); returns the
+    previous one."""
+    prev = lib().srdl_wcoj_jit_set_mode(JIT_MODES[mode])
+    return {v: k for k, v in JIT_MODES.items()}[prev]
+
+
+def jit_wait():
+    """Block until the background kernel compiler is idle."""
+    lib().srdl_wcoj_jit_wait()
 
 
 def device() -> torch.device:

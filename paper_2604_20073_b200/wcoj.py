@@ -109,9 +109,11 @@ def prepare(plan: JoinPlan, store, interner, derived=None) -> Prepared:
     return Prepared(plan, rels, segs, ok, head, len(interner), derived)
 
 
-def encode_plan(prep: Prepared) -> dev.PlanDesc:
-    """JoinPlan + resolved segments -> the fixed-size srdl_plan descriptor."""
-    plan = prep.plan
+def encode_shape(plan: JoinPlan, head_resolved=None) -> dev.PlanDesc:
+    """The static part of the srdl_plan descriptor: depth, atoms, which index
+    columns every atom binds at every level, negations, the head projection.
+    It is all the per-plan kernel compiler (csrc/wcoj_jit.cu) needs; index
+    pointers, row ranges and segment counts are filled in by encode_plan."""
     if plan.depth > dev.MAX_LEVELS or len(plan.atoms) > dev.MAX_ATOMS:
         raise InternalError(f"plan {plan.plan_id}: {plan.depth} variables / {len(plan.atoms)} atoms "
                             f"exceed the device limits ({dev.MAX_LEVELS}/{dev.MAX_ATOMS})")
@@ -123,7 +125,9 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
     d.outer = plan.outer_atom if plan.outer_atom is not None else dev.NO_ATOM
     d.inner = plan.inner_atom if plan.inner_atom is not None else dev.NO_ATOM
     d.head_arity = plan.head_arity
-    for h, (is_var, x) in enumerate(prep.head_resolved):
+    heads = head_resolved if head_resolved is not None else [(kind == VAR, x if kind == VAR else 0)
+                                                           for kind, x in plan.head_cols]
+    for h, (is_var, x) in enumerate(heads):
         d.head_level[h] = x if is_var else -1
         d.head_const[h] = 0 if is_var else x
     for lvl, specs in enumerate(plan.narrow_specs):
@@ -152,6 +156,22 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
         if pa.arity > dev.MAX_COLS:
             raise InternalError(f"relation {pa.relation}: arity {pa.arity} > {dev.MAX_COLS}")
         ad = d.atom[a]
+        ad.negated = int(pa.negated)
+        ad.arity = pa.arity
+        ad.nconst = pa.n_const
+        ad.check_level = pa.check_level
+        for lvl, cols in pa.levels_with_columns().items():
+            ad.lvl_col[lvl] = cols[0]
+            ad.lvl_ncol[lvl] = len(cols)
+    return d
+
+
+def encode_plan(prep: Prepared) -> dev.PlanDesc:
+    """JoinPlan + resolved segments -> the fixed-size srdl_plan descriptor."""
+    plan = prep.plan
+    d = encode_shape(plan, prep.head_resolved)
+    for a, pa in enumerate(plan.atoms):
+        ad = d.atom[a]
         src = prep.segs[a]
         ad.nseg = len(src)
         for s, (rows, lo, hi) in enumerate(src):
@@ -175,14 +195,22 @@ def encode_plan(prep: Prepared) -> dev.PlanDesc:
                 if dense is not None:
                     ad.doff = dense.data_ptr()
                     ad.dn = prep.n_ids
-        ad.negated = int(pa.negated)
-        ad.arity = pa.arity
-        ad.nconst = pa.n_const
-        ad.check_level = pa.check_level
-        for lvl, cols in pa.levels_with_columns().items():
-            ad.lvl_col[lvl] = cols[0]
-            ad.lvl_ncol[lvl] = len(cols)
     return d
+
+
+KERNEL_MODES = {"count": 0, "materialize": 1, "spec": 2}
+
+
+def jit_prepare(plans, mode="spec", wait=False) -> int:
+    """Schedule the per-plan kernels of `plans` (csrc/wcoj_jit.cu: NVRTC on
+    the background compiler threads, disk-cached) so they are ready before
+    the first iterations need them; wait=True blocks until they are built.
+    Returns how many of the plans have one ready (0 with the JIT off)."""
+    plans = [p for p in plans if p.depth]
+    if not plans:
+        return 0
+    arr = (dev.PlanDesc * len(plans))(*[encode_shape(p) for p in plans])
+    return dev.lib().srdl_wcoj_jit_prepare(arr, len(plans), KERNEL_MODES[mode], int(wait))
 
 
 def hist_covers(rel, rows) -> bool:

@@ -13,6 +13,12 @@ for p in (ROOT, HERE):
 
 GOLDEN = os.path.join(HERE, "golden")
 
+# The per-rule kernel compiler (csrc/wcoj_jit.cu) is off for the bulk of the
+# suite: hundreds of small golden programs would each schedule NVRTC builds
+# that finish after their test. tests/test_gpu_jit.py and the BASELINE-size
+# parity tests turn it on (fixture `jit`) and compare both kernel families.
+os.environ.setdefault("SRDL_JIT", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libsrdl.so")
@@ -30,6 +36,18 @@ def load_golden(name):
 @pytest.fixture(scope="session")
 def golden():
     return load_golden
+
+
+@pytest.fixture
+def jit():
+    """Per-rule kernels on, compiled on first use (synchronously)."""
+    from paper_2604_20073_b200 import device as dev
+
+    prev = dev.jit_mode("sync")
+    try:
+        yield dev
+    finally:
+        dev.jit_mode(prev)
 
 
 @pytest.fixture

@@ -51,31 +51,45 @@ def test_rmat_device_generator_matches_host_mirror():
         assert np.array_equal(got, want), (scale, n, seed)
 
 
+@pytest.mark.parametrize("kernels", ["per-rule", "generic"])
 @pytest.mark.parametrize("name", ["tc", "triangle", "sg", "andersen", "doop"])
-def test_baseline_config_full_size_digest(name):
+def test_baseline_config_full_size_digest(name, kernels):
+    """kernels: "per-rule" = the NVRTC-compiled kernel of every plan (the
+    production path, built before the solve), "generic" = the plan-class
+    kernels compiled into libsrdl.so."""
     from paper_2604_20073_b200 import Engine, parse
+    from paper_2604_20073_b200 import device as dev
     from paper_2604_20073_b200.fixpoint import release_arenas
 
     want = _digests().get(name)
     if want is None:
         pytest.fail(f"no committed oracle digest for {name}: run tests/golden/make_baseline_digests.py {name}")
     wl = _facts(name)
-    eng = Engine(parse(wl.program), schedule="stream")
-    for k, v in wl.device_facts().items():
-        eng.load_columns(k, v)
-    summary = eng.solve()
-    for rel, d in want["edb"].items():
-        assert digest(eng.relation_columns(rel).cpu().numpy()) == d, (name, "EDB", rel)
-    for rel, d in want["idb"].items():
-        assert summary.relations[rel] == d["n"], (name, rel)
-        got = digest(eng.relation_columns(rel).cpu().numpy())
-        assert got == d, (name, rel)
-    rounds = [s.iterations for s in summary.strata if s.recursive]
-    if want.get("recursive_rounds") and not parse(wl.program).splits:
-        assert sorted(rounds) == sorted(want["recursive_rounds"]), name
-    del eng
-    torch.cuda.synchronize()
-    release_arenas()
+    prev = dev.jit_mode("async" if kernels == "per-rule" else "off")
+    try:
+        eng = Engine(parse(wl.program), schedule="stream")  # schedules the per-rule kernels
+        if kernels == "per-rule":
+            dev.jit_wait()
+            dev.jit_mode("sync")  # anything not built yet (materialize re-walks) compiles on first use
+        for k, v in wl.device_facts().items():
+            eng.load_columns(k, v)
+        summary = eng.solve()
+        for rel, d in want["edb"].items():
+            assert digest(eng.relation_columns(rel).cpu().numpy()) == d, (name, "EDB", rel)
+        for rel, d in want["idb"].items():
+            assert summary.relations[rel] == d["n"], (name, rel)
+            got = digest(eng.relation_columns(rel).cpu().numpy())
+            assert got == d, (name, rel)
+        rounds = [s.iterations for s in summary.strata if s.recursive]
+        if want.get("recursive_rounds") and not parse(wl.program).splits:
+            assert sorted(rounds) == sorted(want["recursive_rounds"]), name
+        del eng
+        torch.cuda.synchronize()
+        release_arenas()
+        if kernels == "per-rule":
+            assert dev.jit_stats()["failures"] == 0
+    finally:
+        dev.jit_mode(prev)
 
 
 def test_triangle_heaviest_root_keys_row_exact():
@@ -104,6 +118,6 @@ def test_triangle_heaviest_root_keys_row_exact():
     eng.solve()
     rows = eng.relation_columns("Triangle")
     sel = torch.isin(rows[0].view(torch.int32), torch.from_numpy(keys.view(np.int32)).cuda())
-    got = rows[:, sel].cpu().numpy().T
+    got = rows.view(torch.int32)[:, sel].cpu().numpy().view(np.uint32).T
     assert len(want) > 1_000_000
     assert np.array_equal(got, want)

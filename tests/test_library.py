@@ -23,7 +23,7 @@ def lib():
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|uint64_t|const char \*)\s*(srdl_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|uint64_t|const char \*)\s*(srdl_\w+)\(", text, re.M)))
 
 
 def test_every_declared_symbol_is_exported(lib):
@@ -86,3 +86,21 @@ def test_col_ptrs_single_row_any_stride():
     assert ptrs[2] - ptrs[0] == 2 * 5 * 4
     with pytest.raises(Exception):
         dev.col_ptrs(torch.zeros((5, 3), dtype=torch.int32).t())
+
+
+def test_per_rule_kernels_compile_for_sm100a(lib):
+    """The generated per-plan kernel source compiles with NVRTC for sm_100a
+    (no GPU needed): the triangle's depth-3 plan and DOOP's deepest rule."""
+    from paper_2604_20073_b200 import compile_program, parse, suites
+    from paper_2604_20073_b200.wcoj import encode_shape
+
+    tri = compile_program(parse(suites.TRIANGLE_PROGRAM)).strata[-1].plans[0]
+    doop = compile_program(parse(suites.BASELINE_PROGRAMS["doop"][0]))
+    deep = max((p for st in doop.strata for p in st.plans), key=lambda p: p.depth)
+    for plan, mode in ((tri, 2), (deep, 2), (tri, 1)):
+        nb = ctypes.c_uint64(0)
+        rc = lib.srdl_wcoj_jit_compile_check(ctypes.byref(encode_shape(plan)), mode, ctypes.byref(nb))
+        if rc == 2:
+            pytest.skip("NVRTC unavailable")
+        assert rc == 0, lib.srdl_last_error().decode()
+        assert nb.value > 10_000
