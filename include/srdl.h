@@ -331,6 +331,17 @@ void srdl_wcoj_jit_stats(uint64_t *out);
 int srdl_route_rows(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
                     uint32_t world, uint32_t *const *out, uint64_t *counts, void *stream);
 
+/* The send buffer of one all-to-all exchange, without a host round trip:
+ * rows grouped by the owner of column `key_col` (stable within a rank),
+ * written row-major (send[i * arity + c], n * arity words), and the rows per
+ * rank into counts_dev[world] (device memory). Replaces srdl_route_rows
+ * (one pass and one host read per rank) on the exchange path. */
+int srdl_route_pack(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                    uint32_t world, uint32_t *send, uint64_t *counts_dev, void *stream);
+
+/* Received row-major rows (recv[i * arity + c]) back to `arity` columns. */
+int srdl_unpack_rows(const uint32_t *recv, uint32_t arity, uint64_t n, uint32_t *const *out, void *stream);
+
 /* Keep the rows whose column `key_col` is owned by `rank` (stable);
  * *n_out (host) = rows kept. out has capacity n. */
 int srdl_filter_owned(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,

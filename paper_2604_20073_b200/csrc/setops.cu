@@ -346,6 +346,52 @@ static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, 
     return K;
 }
 
+// ---- packed exchange buffers (multi-GPU all-to-all, dist.py)
+
+__global__ void owner_keys(const uint32_t *__restrict__ col, uint64_t n, uint32_t world,
+                           uint64_t *__restrict__ keys, uint32_t *__restrict__ idx) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        keys[i] = owner_of(__ldg(col + i), world);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// counts[r] = rows owned by rank r (keys sorted by owner)
+__global__ void owner_counts(const uint64_t *__restrict__ keys, uint64_t n, uint32_t world,
+                             uint64_t *__restrict__ counts) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= world) return;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {  // first key >= r
+        const uint64_t m = (lo + hi) >> 1;
+        if (keys[m] < r) lo = m + 1; else hi = m;
+    }
+    uint64_t a = lo;
+    hi = n;
+    while (lo < hi) {  // first key > r
+        const uint64_t m = (lo + hi) >> 1;
+        if (keys[m] <= r) lo = m + 1; else hi = m;
+    }
+    counts[r] = lo - a;
+}
+
+// send[i * arity + c] = cols[c][idx[i]]: row-major rows, grouped by owner
+__global__ void pack_rows(Cols cols, uint32_t arity, const uint32_t *__restrict__ idx, uint64_t n,
+                          uint32_t *__restrict__ send) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = __ldg(idx + i);
+        for (uint32_t c = 0; c < arity; ++c) send[i * arity + c] = __ldg(cols.c[c] + r);
+    }
+}
+
+__global__ void unpack_rows(const uint32_t *__restrict__ recv, uint32_t arity, uint64_t n, MutCols out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        for (uint32_t c = 0; c < arity; ++c) out.c[c][i] = __ldg(recv + i * arity + c);
+}
+
 }  // namespace srdl
 
 using namespace srdl;
@@ -357,6 +403,7 @@ static void histogram_union_impl(const uint32_t *col, uint64_t n, const uint32_t
 
 
 extern "C" {
+
 
 int srdl_merge(const uint32_t *const *a, uint64_t na, const uint32_t *const *b, uint64_t nb,
                uint32_t arity, uint32_t *const *out, void *stream) {
@@ -563,6 +610,39 @@ static uint64_t route_one(const Cols &in, uint32_t arity, uint64_t n, uint32_t k
     SRDL_CUDA(cudaMemcpyAsync(&cnt, total.as<uint32_t>(), sizeof(cnt), cudaMemcpyDeviceToHost, s));
     SRDL_CUDA(cudaStreamSynchronize(s));
     return cnt;
+}
+
+int srdl_route_pack(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,
+                    uint32_t world, uint32_t *send, uint64_t *counts_dev, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(world >= 1 && world <= 256 && key_col < arity && arity <= SRDL_MAX_COLS,
+                     "bad routing arguments");
+        SRDL_REQUIRE(n < (1ull << 32), "route: too many rows");
+        cudaStream_t s = (cudaStream_t)stream;
+        if (n == 0) {
+            SRDL_CUDA(cudaMemsetAsync(counts_dev, 0, world * sizeof(uint64_t), s));
+            return;
+        }
+        Scratch keys(n * sizeof(uint64_t), s), idx(n * sizeof(uint32_t), s);
+        owner_keys<<<stride_grid(n), kThreads, 0, s>>>(cols[key_col], n, world, keys.as<uint64_t>(),
+                                                       idx.as<uint32_t>());
+        SRDL_CHECK_LAUNCH();
+        // one stable radix pass on the owner (8 bits): rows grouped by rank,
+        // in their original order within a rank
+        radix_sort(keys.as<uint64_t>(), idx.as<uint32_t>(), n, 8, s);
+        owner_counts<<<(world + 255) / 256, 256, 0, s>>>(keys.as<uint64_t>(), n, world, counts_dev);
+        SRDL_CHECK_LAUNCH();
+        pack_rows<<<stride_grid(n), kThreads, 0, s>>>(make_cols(cols, arity), arity, idx.as<uint32_t>(), n, send);
+        SRDL_CHECK_LAUNCH();
+    });
+}
+
+int srdl_unpack_rows(const uint32_t *recv, uint32_t arity, uint64_t n, uint32_t *const *out, void *stream) {
+    return guarded([&] {
+        if (n == 0) return;
+        unpack_rows<<<stride_grid(n), kThreads, 0, (cudaStream_t)stream>>>(recv, arity, n, make_mut(out, arity));
+        SRDL_CHECK_LAUNCH();
+    });
 }
 
 int srdl_route_rows(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t key_col,

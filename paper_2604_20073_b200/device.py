@@ -195,6 +195,11 @@ _SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p],
     ),
+    "srdl_route_pack": (
+        C.c_int,
+        [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
+    "srdl_unpack_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]),
     "srdl_filter_owned": (
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
@@ -611,6 +616,25 @@ def route_rows(rows: torch.Tensor, key_col: int, world: int):
     check(lib().srdl_route_rows(col_ptrs(rows), arity, n, key_col, world, col_ptrs(out), counts,
                                 stream_handle()), "route_rows")
     return out, [int(counts[r]) for r in range(world)]
+
+
+def route_pack(rows: torch.Tensor, key_col: int, world: int):
+    """(row-major int32 send buffer grouped by owner of column key_col,
+    per-rank row counts as an int64 device tensor) — no host round trip."""
+    arity, n = rows.shape
+    send = torch.empty(n * arity, dtype=torch.int32, device=device())
+    counts = torch.empty(world, dtype=torch.int64, device=device())
+    check(lib().srdl_route_pack(col_ptrs(rows) if n else None, arity, n, key_col, world,
+                                send.data_ptr() if n else None, counts.data_ptr(), stream_handle()), "route_pack")
+    return send, counts
+
+
+def unpack_rows(recv: torch.Tensor, arity: int, n: int) -> torch.Tensor:
+    """Row-major received rows -> (arity, n) columns."""
+    out = empty_rows(arity, n)
+    if n:
+        check(lib().srdl_unpack_rows(recv.data_ptr(), arity, n, col_ptrs(out), stream_handle()), "unpack_rows")
+    return out
 
 
 def filter_owned(rows: torch.Tensor, key_col: int, world: int, rank: int) -> torch.Tensor:

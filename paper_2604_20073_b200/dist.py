@@ -75,6 +75,10 @@ class DistContext:
         self.backend = str(td.get_backend(group))
         # gloo collectives run on host tensors (tests); NCCL on device memory
         self.staged = self.backend != "nccl"
+        # payload this rank sent to other ranks (all-to-all rows, all-gather
+        # rows), and the number of exchanges — DESIGN.md's per-iteration table
+        self.sent_bytes = 0
+        self.exchanges = 0
 
     def _dev(self):
         return torch.device("cpu") if self.staged else dev.device()
@@ -98,9 +102,26 @@ class DistContext:
         return recv.to(rows.device).t().contiguous().view(torch.uint32)
 
     def route(self, rows: torch.Tensor, key_col: int) -> torch.Tensor:
-        """Rows delivered to the owner of their column key_col."""
-        routed, counts = dev.route_rows(rows, key_col, self.world)
-        return self.all_to_all_rows(routed, counts)
+        """Rows delivered to the owner of their column key_col: one packing
+        kernel writes the row-major send buffer grouped by owner and the
+        per-rank counts on the device (srdl_route_pack), the counts are
+        exchanged, ONE host read of (sent, received) counts sizes the
+        receive buffer, one all-to-all moves the rows and srdl_unpack_rows
+        restores the columns."""
+        arity, n = rows.shape
+        send, counts = dev.route_pack(rows, key_col, self.world)
+        cdev = self._dev()
+        counts_c = counts.to(cdev)
+        recv_n = torch.empty_like(counts_c)
+        self.td.all_to_all_single(recv_n, counts_c, group=self.group)
+        both = torch.cat([counts_c, recv_n]).tolist()  # the exchange's one host read
+        sent, got = both[:self.world], both[self.world:]
+        recv = torch.empty(sum(got) * arity, dtype=torch.int32, device=cdev)
+        self.td.all_to_all_single(recv, send.to(cdev), [g * arity for g in got], [c * arity for c in sent],
+                                  group=self.group)
+        self.sent_bytes += 4 * arity * (sum(sent) - sent[self.rank])
+        self.exchanges += 1
+        return dev.unpack_rows(recv.to(rows.device), arity, sum(got))
 
     def all_gather_rows(self, rows: torch.Tensor) -> torch.Tensor:
         """Concatenation (rank order) of every rank's rows."""
@@ -108,12 +129,14 @@ class DistContext:
         cdev = self._dev()
         sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(self.world)]
         self.td.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=cdev), group=self.group)
-        sizes = [int(s.item()) for s in sizes]
+        sizes = torch.cat(sizes).tolist()  # one host read
         top = max(sizes) if sizes else 0
         mine = torch.zeros((top, arity), dtype=torch.int32, device=cdev)
         if n:
             mine[:n] = rows.view(torch.int32).t().to(cdev)
         parts = [torch.empty((top, arity), dtype=torch.int32, device=cdev) for _ in range(self.world)]
         self.td.all_gather(parts, mine, group=self.group)
+        self.sent_bytes += 4 * arity * n * (self.world - 1)
+        self.exchanges += 1
         got = torch.cat([p[:s] for p, s in zip(parts, sizes)]) if sizes else mine[:0]
         return got.to(rows.device).t().contiguous().view(torch.uint32)

@@ -14,6 +14,7 @@ Fixtures:
   plans.json        compiled plan structure for a corpus of programs
   partitions.json   WorkPartition prefix/bounds/kappa/spans/decode samples
   storage.json      sort_dedup / compute_delta / merge(head, body) / histogram
+  merges.json.gz    1000 merge sequences (the acceptance suite's criterion 7)
   fixpoints.json.gz seeded fixpoints: facts, every relation's rows, strata
   joins.json.gz     random multi-way joins (reference random_join_case)
   errors.json       program texts and the ProgramError message they raise
@@ -207,6 +208,38 @@ def gen_storage():
     dump("storage.json", out)
 
 
+def gen_merges():
+    """1000 random merge sequences (pkg/tests/test_acceptance.py:325-357,
+    criterion 7: arity 1-3, flush 0 / 3 / 4096, 2-6 batches of up to 40 rows
+    over 25 values): head, body and histogram after every merge."""
+    rng = random.Random(99)
+    seqs = []
+    while len(seqs) < 1000:
+        arity = rng.randint(1, 3)
+        flush = rng.choice([0, 3, 4096])
+        order = tuple(rng.sample(range(arity), arity))
+        rel = ColumnarRelation.empty(arity, order)
+        contents = set()
+        steps = []
+        for _ in range(rng.randint(2, 6)):
+            batch = {tuple(rng.randrange(25) for _ in range(arity)) for _ in range(rng.randrange(40))}
+            ordered = sorted(tuple(row[a] for a in order) for row in batch)
+            fresh = [row for row in ordered if row not in contents]
+            contents.update(fresh)
+            rel = rel.merge_delta(rowops.from_tuples(fresh, arity), flush_limit=flush)
+            rel.check_invariants()
+            steps.append({
+                "delta": fresh,
+                "head": rowops.as_tuples(rel.head),
+                "body": rowops.as_tuples(rel.body),
+                "hist_keys": rel.hist.keys.tolist(),
+                "hist_degrees": rel.hist.degrees.tolist(),
+                "hist_prefix": rel.hist.prefix.tolist(),
+            })
+        seqs.append({"arity": arity, "flush": flush, "order": list(order), "steps": steps})
+    dump("merges.json.gz", seqs, gz=True)
+
+
 def relation_dump(engine, program):
     return {name: [list(r) for r in engine.relation_rows(name)] for name in program.declarations}
 
@@ -233,7 +266,10 @@ def fixpoint_record(name, src, facts, **kw):
 
 def gen_fixpoints():
     records = []
-    for kind, count in (("tc", 30), ("sg", 30), ("andersen", 30), ("negation", 30)):
+    # 100 instances per program, as the reference acceptance suite runs
+    # (pkg/tests/test_acceptance.py:145-178; its seeds are hash((kind, i)),
+    # randomised per process, so ours are f"{kind}-{i}" over the same shapes)
+    for kind, count in (("tc", 100), ("sg", 100), ("andersen", 100), ("negation", 100)):
         for index in range(count):
             rng = random.Random(f"{kind}-{index}")
             if kind == "tc":
@@ -336,11 +372,16 @@ def small_facts_for(name, rng):
 
 def gen_joins():
     cases = []
-    for case in range(150):
+    # 500 joins at p in {1, 2, 8}, as pkg/tests/test_acceptance.py:84-103
+    for case in range(500):
         program, facts, head_vars = ref_util.random_join_case(seed=20_000 + case)
         engine = ref_util.seeded_engine(program, facts)
         plan = ref_util.plan_for_head(engine, "Out")
-        out = execute_plan(plan, engine.store, 3, engine.interner)
+        emitted = {}
+        for p in (1, 2, 8):
+            out = execute_plan(plan, engine.store, p, engine.interner)
+            emitted[p] = sorted(tuple(int(c[i]) for c in out) for i in range(len(out[0])))
+        assert emitted[1] == emitted[2] == emitted[8], case
         rows = sorted({tuple(engine.interner.text(int(c[i])) for c in out) for i in range(len(out[0]))})
         src = "\n".join(
             [f".decl {n}({', '.join(f'c{i}:symbol' for i in range(a))})" for n, a in program.declarations.items()]
@@ -355,6 +396,7 @@ def gen_joins():
                 "facts": {k: [list(r) for r in v] for k, v in facts.items()},
                 "out": [list(r) for r in rows],
                 "emitted": len(out[0]),
+                "ps": [1, 2, 8],
             }
         )
     dump("joins.json.gz", cases, gz=True)
@@ -402,6 +444,7 @@ if __name__ == "__main__":
     gen_plans()
     gen_partitions()
     gen_storage()
+    gen_merges()
     gen_errors()
     gen_joins()
     gen_fixpoints()

@@ -48,7 +48,8 @@ def test_compute_delta_golden(dev, golden):
 def test_merge_sequences_golden(dev, golden):
     from paper_2604_20073_b200.columns import ColumnarRelation, as_tuples
 
-    for case in golden("storage.json")["merge"]:
+    # storage.json's 80 sequences + the acceptance suite's 1000 (merges.json.gz)
+    for case in golden("storage.json")["merge"] + golden("merges.json.gz"):
         a = case["arity"]
         rel = ColumnarRelation.empty(a, case["order"])
         for step in case["steps"]:

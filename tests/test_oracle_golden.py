@@ -55,7 +55,7 @@ def test_oracle_storage_matches_reference(golden):
         got = ost.compute_delta(ost.as_rows(case["new"], a), ost.as_rows(case["head"], a),
                                 ost.as_rows(case["body"], a))
         assert got.tolist() == case["out"]
-    for case in st["merge"]:
+    for case in st["merge"] + golden("merges.json.gz"):
         rel = ost.HeadBody(case["arity"], case["flush"])
         for step in case["steps"]:
             rel.merge_delta(ost.as_rows(step["delta"], case["arity"]))
