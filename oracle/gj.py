@@ -128,14 +128,29 @@ class _Src:
 
 
 def variable_order(rule, delta_pos=None) -> list:
+    """Delta atom's variables first, then repeatedly the first-occurring
+    variable that shares a positive atom with an already ordered one (the
+    next level is always constrained by a bound neighbour; a variable
+    reachable only through an unbound one would be enumerated over its whole
+    domain), falling back to first occurrence for disconnected bodies. Any
+    order gives the same relation; this one keeps the oracle's work close
+    to the join's output size."""
     order = []
     if delta_pos is not None:
         order += [v for v in rule.body[delta_pos].variables() if v not in order]
-    for a in rule.body:
-        if not a.negated:
-            for v in a.variables():
-                if v not in order:
-                    order.append(v)
+    positive = [a for a in rule.body if not a.negated]
+    pending = []
+    for a in positive:
+        for v in a.variables():
+            if v not in order and v not in pending:
+                pending.append(v)
+    while pending:
+        bound = set(order)
+        pick = next((v for v in pending
+                     if any(v in a.variables() and bound.intersection(a.variables()) for a in positive)),
+                    pending[0])
+        order.append(pick)
+        pending.remove(pick)
     return order
 
 

@@ -17,49 +17,78 @@ constexpr int kRadixBits = 8;
 constexpr int kBins = 1 << kRadixBits;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWarpChunk = 32 * kItems;
+constexpr int kMaxPasses = 8;  // 64-bit keys
 
-__device__ __forceinline__ uint64_t tile_index(int w, int r, int l) {
-    return (uint64_t)blockIdx.x * kTile + (uint64_t)w * kWarpChunk + r * 32 + l;
+__device__ __forceinline__ uint64_t tile_index(uint64_t tile, int w, int r, int l) {
+    return tile * kTile + (uint64_t)w * kWarpChunk + r * 32 + l;
 }
 
-// Per-block digit histogram, written digit-major: counts[d * nblocks + b].
+// Onesweep LSD radix sort (decoupled look-back, Merrill & Garland's single-
+// pass prefix scan applied per digit): one histogram pass over the keys
+// counts the digits of every pass at once; each pass then reads and writes
+// every key exactly once — a tile ranks its keys, publishes its per-digit
+// counts, looks back over the preceding tiles' published counts for its
+// global offsets and scatters. Per pass: 8 B read + 8 B written per key
+// (+ 4 + 4 B of row permutation), instead of the 8 + 8 + 8 B of a separate
+// histogram read, and one launch instead of three.
+
+// ghist[p * kBins + d] += number of keys whose pass-p digit is d
 __global__ void __launch_bounds__(kThreads)
-    radix_hist(const uint64_t *__restrict__ keys, uint64_t n, int shift, uint32_t *counts,
-               const int *__restrict__ unsorted) {
-    if (unsorted && *unsorted == 0) return;  // input already in order: pass skipped
-    __shared__ uint32_t h[kWarps][kBins];
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&h[0][0])[i] = 0;
+    radix_hist_all(const uint64_t *__restrict__ keys, uint64_t n, int passes, uint32_t *__restrict__ ghist,
+                   const int *__restrict__ unsorted) {
+    if (unsorted && *unsorted == 0) return;  // input already in order: the sort is skipped
+    __shared__ uint32_t h[kMaxPasses][kBins];
+    for (int i = threadIdx.x; i < kMaxPasses * kBins; i += kThreads) (&h[0][0])[i] = 0;
     __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < kItems; ++r) {
-        uint64_t i = tile_index(w, r, l);
-        if (i < n) atomicAdd(&h[w][(keys[i] >> shift) & (kBins - 1)], 1u);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = __ldcs(keys + i);
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (p * kRadixBits)) & (kBins - 1)], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < kBins; d += kThreads) {
-        uint32_t t = 0;
+    for (int i = threadIdx.x; i < passes * kBins; i += kThreads) {
+        const uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(ghist + i, v);
+    }
+}
+
+// per pass: exclusive scan of the digit counts (one warp per pass)
+__global__ void radix_digit_starts(uint32_t *hist, int passes, const int *__restrict__ unsorted) {
+    if (unsorted && *unsorted == 0) return;
+    const int p = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (p >= passes) return;
+    uint32_t *h = hist + p * kBins;
+    uint32_t carry = 0;
+    for (int base = 0; base < kBins; base += 32) {
+        const uint32_t v = h[base + l];
+        uint32_t incl = v;
 #pragma unroll
-        for (int k = 0; k < kWarps; ++k) t += h[k][d];
-        counts[(uint64_t)d * gridDim.x + blockIdx.x] = t;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (l >= o) incl += y;
+        }
+        h[base + l] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
-// Stable scatter: rank within the tile via warp match + per-warp counters,
-// then the tile is reordered by digit in shared memory and written out with
-// consecutive threads storing consecutive positions of each digit's run
-// (coalesced; a direct per-key store would touch one sector per key).
+// look-back status word per (tile, digit): flag in the top two bits
+constexpr uint64_t kFlagAgg = 1ull << 62;  // this tile's own count is published
+constexpr uint64_t kFlagInc = 2ull << 62;  // inclusive prefix through this tile
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
 template <bool HAS_VALS>
-constexpr size_t scatter_smem() {
+constexpr size_t onesweep_smem() {
     return (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0) + (size_t)kWarps * kBins * 4 +
-           (size_t)kBins * 8 + 64 * 4;
+           (size_t)kBins * 8 + 64 * 4 + 16;
 }
 
 template <bool HAS_VALS>
-__global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 resident tiles per SM
-    radix_scatter(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n,
-                  int shift, const uint32_t *__restrict__ offsets, uint64_t *__restrict__ keys_out,
-                  uint32_t *__restrict__ vals_out, const int *__restrict__ unsorted) {
+__global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)
+    onesweep_pass(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n, int shift,
+                  const uint32_t *__restrict__ starts, uint64_t *status, uint32_t *tile_ticket,
+                  uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                  const int *__restrict__ unsorted) {
     if (unsorted && *unsorted == 0) return;
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *skeys = (uint64_t *)sm;
@@ -67,21 +96,26 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 r
     uint32_t(*cnt)[kBins] = (uint32_t(*)[kBins])(sm + (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0));
     int64_t *gbase = (int64_t *)((unsigned char *)cnt + (size_t)kWarps * kBins * 4);
     uint32_t *wsum = (uint32_t *)(gbase + kBins);  // [kWarps] scan carries
+    uint32_t *tile_slot = wsum + 64;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    // tiles are numbered in the order blocks start, so every tile a block
+    // looks back on has started (forward progress of the look-back)
+    if (threadIdx.x == 0) *tile_slot = atomicAdd(tile_ticket, 1u);
     for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&cnt[0][0])[i] = 0;
     __syncthreads();
+    const uint64_t tile = *tile_slot;
     uint64_t k[kItems];
     uint32_t v[kItems];
     uint32_t rank[kItems];
     const uint32_t lt = (1u << l) - 1u;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
-        uint64_t i = tile_index(w, r, l);
-        bool ok = i < n;
-        k[r] = ok ? keys[i] : 0;
-        if (HAS_VALS) v[r] = ok ? vals[i] : 0;
-        uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint64_t i = tile_index(tile, w, r, l);
+        const bool ok = i < n;
+        k[r] = ok ? __ldcs(keys + i) : 0;
+        if (HAS_VALS) v[r] = ok ? __ldcs(vals + i) : 0;
+        const uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t before = 0;
         if (ok) before = cnt[w][d];
         __syncwarp();
@@ -91,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 r
     }
     __syncthreads();
     // digit d (one per thread, kThreads == kBins): per-warp exclusive offsets
-    // within the digit, then a block-wide exclusive scan of the digit totals
+    // within the digit, the tile's digit total, a block scan of the totals
     static_assert(kThreads == kBins, "one thread per digit");
     const int d = threadIdx.x;
     uint32_t total = 0;
@@ -101,7 +135,26 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 r
         cnt[q][d] = total;
         total += c;
     }
-    uint32_t incl = total;  // inclusive scan of totals across the block
+    // publish this tile's count, then look back for the digit's prefix
+    uint64_t *st = status + tile * kBins + d;
+    if (tile == 0) {
+        *(volatile uint64_t *)st = kFlagInc | total;
+    } else {
+        *(volatile uint64_t *)st = kFlagAgg | total;
+    }
+    uint64_t excl = 0;
+    if (tile > 0) {
+        int64_t t = (int64_t)tile - 1;
+        while (true) {
+            uint64_t s = *(volatile uint64_t *)(status + (uint64_t)t * kBins + d);
+            if ((s & ~kValMask) == 0) continue;  // predecessor not published yet
+            excl += s & kValMask;
+            if (s & kFlagInc) break;
+            --t;
+        }
+        *(volatile uint64_t *)st = kFlagInc | (excl + total);
+    }
+    uint32_t incl = total;  // block-wide inclusive scan of the digit totals
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -114,11 +167,11 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 r
     const uint32_t local_start = carry + incl - total;
 #pragma unroll
     for (int q = 0; q < kWarps; ++q) cnt[q][d] += local_start;
-    gbase[d] = (int64_t)offsets[(uint64_t)d * gridDim.x + blockIdx.x] - (int64_t)local_start;
+    gbase[d] = (int64_t)starts[d] + (int64_t)excl - (int64_t)local_start;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
-        uint64_t i = tile_index(w, r, l);
+        const uint64_t i = tile_index(tile, w, r, l);
         if (i < n) {
             const uint32_t dd = (uint32_t)((k[r] >> shift) & (kBins - 1));
             const uint32_t lpos = cnt[w][dd] + rank[r];
@@ -127,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)  // keys only: 3 r
         }
     }
     __syncthreads();
-    const uint64_t base = (uint64_t)blockIdx.x * kTile;
+    const uint64_t base = tile * kTile;
     const uint32_t here = n - base < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
     for (uint32_t i = threadIdx.x; i < here; i += kThreads) {
         const uint64_t key = skeys[i];
@@ -155,31 +208,45 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
     if (n <= 1 || bits == 0) return;
     SRDL_REQUIRE(n < (1ull << 32), "radix_sort: %llu rows exceeds the 32-bit rank space",
                  (unsigned long long)n);
-    const uint64_t blocks = (n + kTile - 1) / kTile;
+    const uint64_t tiles = (n + kTile - 1) / kTile;
     const int passes = (int)((bits + kRadixBits - 1) / kRadixBits);
+    SRDL_REQUIRE(passes <= kMaxPasses, "radix_sort: %u bits", bits);
     static uint64_t raised = 0;
     if (first_use_on_device(&raised)) {  // the reorder tile needs more than the 48 KB default
-        SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)scatter_smem<true>()));
-        SRDL_CUDA(cudaFuncSetAttribute(radix_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)scatter_smem<false>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<true>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<false>()));
     }
     Scratch kalt(n * sizeof(uint64_t), s);
     Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);
-    Scratch counts(blocks * kBins * sizeof(uint32_t), s);
+    // digit counts of every pass and one tile ticket per pass (zeroed once),
+    // the look-back status of every (tile, digit) of the running pass
+    // (zeroed before each pass, stream-ordered after the previous one)
+    const size_t hist_bytes = (size_t)kMaxPasses * kBins * sizeof(uint32_t);
+    const size_t ticket_bytes = (size_t)kMaxPasses * sizeof(uint32_t);
+    const size_t status_bytes = (size_t)tiles * kBins * sizeof(uint64_t);
+    Scratch meta(hist_bytes + ticket_bytes, s);
+    Scratch status(status_bytes, s);
+    uint32_t *hist = meta.as<uint32_t>();
+    uint32_t *tickets = hist + kMaxPasses * kBins;
+    SRDL_CUDA(cudaMemsetAsync(hist, 0, hist_bytes + ticket_bytes, s));
+    radix_hist_all<<<stride_grid(n), kThreads, 0, s>>>(keys, n, passes, hist, unsorted);
+    SRDL_CHECK_LAUNCH();
+    radix_digit_starts<<<1, 32 * kMaxPasses, 0, s>>>(hist, passes, unsorted);
+    SRDL_CHECK_LAUNCH();
     uint64_t *kin = keys, *kout = kalt.as<uint64_t>();
     uint32_t *vin = vals, *vout = vals ? valt.as<uint32_t>() : nullptr;
     for (int p = 0; p < passes; ++p) {
-        int shift = p * kRadixBits;
-        radix_hist<<<(unsigned)blocks, kThreads, 0, s>>>(kin, n, shift, counts.as<uint32_t>(), unsorted);
-        SRDL_CHECK_LAUNCH();
-        exclusive_scan_u32(counts.as<uint32_t>(), counts.as<uint32_t>(), blocks * kBins, nullptr, s);
+        const int shift = p * kRadixBits;
+        SRDL_CUDA(cudaMemsetAsync(status.as<uint64_t>(), 0, status_bytes, s));
         if (vals)
-            radix_scatter<true><<<(unsigned)blocks, kThreads, scatter_smem<true>(), s>>>(
-                kin, vin, n, shift, counts.as<uint32_t>(), kout, vout, unsorted);
+            onesweep_pass<true><<<(unsigned)tiles, kThreads, onesweep_smem<true>(), s>>>(
+                kin, vin, n, shift, hist + p * kBins, status.as<uint64_t>(), tickets + p, kout, vout, unsorted);
         else
-            radix_scatter<false><<<(unsigned)blocks, kThreads, scatter_smem<false>(), s>>>(
-                kin, nullptr, n, shift, counts.as<uint32_t>(), kout, nullptr, unsorted);
+            onesweep_pass<false><<<(unsigned)tiles, kThreads, onesweep_smem<false>(), s>>>(
+                kin, nullptr, n, shift, hist + p * kBins, status.as<uint64_t>(), tickets + p, kout, nullptr,
+                unsorted);
         SRDL_CHECK_LAUNCH();
         std::swap(kin, kout);
         std::swap(vin, vout);

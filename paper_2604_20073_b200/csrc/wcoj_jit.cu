@@ -217,10 +217,19 @@ std::string shape_source(const srdl_plan *P, int mode) {
 }
 
 const std::vector<std::string> &compile_options() {
-    static std::vector<std::string> opts = {
-        "--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device",
-        "-I" + paths().csrc,          "-I" + paths().include,
-    };
+    static std::vector<std::string> opts = [] {
+        std::vector<std::string> o = {
+            "--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-default-device",
+            "-I" + paths().csrc,          "-I" + paths().include,
+        };
+        // extra -D options (tuning sweeps, e.g. -DSRDL_MERGE_RATIO=4), space-separated
+        if (const char *e = getenv("SRDL_JIT_DEFINES")) {
+            std::istringstream in(e);
+            std::string tok;
+            while (in >> tok) o.push_back(tok);
+        }
+        return o;
+    }();
     return opts;
 }
 

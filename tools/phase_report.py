@@ -42,6 +42,7 @@ def main():
     for rep in range(2):
         stats = Stats(enabled=not args.kernels)
         eng = Engine(parse(program), schedule=args.schedule, stats=stats)
+        dev.jit_wait()  # the per-rule kernels of the program (scheduled by the Engine) are built
         for k, v in facts.items():
             eng.load_columns(k, v)
         prof = None
