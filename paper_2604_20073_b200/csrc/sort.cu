@@ -144,13 +144,30 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)
     }
     uint64_t excl = 0;
     if (tile > 0) {
+        // windowed look-back: kLook predecessors loaded at once (independent
+        // loads), consumed newest first until an inclusive prefix; a window
+        // restarts at the first tile that has not published yet. A serial
+        // walk made the first wave's look-backs chains of hundreds of
+        // dependent L2 round trips.
+        constexpr int kLook = 8;
         int64_t t = (int64_t)tile - 1;
         while (true) {
-            uint64_t s = *(volatile uint64_t *)(status + (uint64_t)t * kBins + d);
-            if ((s & ~kValMask) == 0) continue;  // predecessor not published yet
-            excl += s & kValMask;
-            if (s & kFlagInc) break;
-            --t;
+            uint64_t sw[kLook];
+#pragma unroll
+            for (int j = 0; j < kLook; ++j)
+                sw[j] = t - j >= 0 ? *(volatile uint64_t *)(status + (uint64_t)(t - j) * kBins + d) : (2ull << 62);  // before tile 0: an empty inclusive prefix
+            int j = 0;
+            bool done = false;
+#pragma unroll
+            for (int q = 0; q < kLook; ++q) {
+                if (done || j != q) continue;
+                if ((sw[q] & ~kValMask) == 0) continue;  // not published yet: retry from here
+                excl += sw[q] & kValMask;
+                ++j;
+                done = (sw[q] & kFlagInc) != 0;
+            }
+            if (done) break;
+            t -= j;
         }
         *(volatile uint64_t *)st = kFlagInc | (excl + total);
     }

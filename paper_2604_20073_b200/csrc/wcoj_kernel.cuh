@@ -94,7 +94,7 @@ constexpr uint32_t kSegs = SRDL_MAX_SEGS;
 #define SRDL_MERGE_MIN 64
 #endif
 #ifndef SRDL_MERGE_RATIO
-#define SRDL_MERGE_RATIO 16
+#define SRDL_MERGE_RATIO 4
 #endif
 constexpr uint32_t kMergeMin = SRDL_MERGE_MIN;
 constexpr uint32_t kMergeRatio = SRDL_MERGE_RATIO;
@@ -464,6 +464,10 @@ __device__ __forceinline__ uint32_t spec_of(const srdl_plan &P, int L, uint32_t 
     return SH::spec(P, L, j);
 }
 
+__device__ __forceinline__ void prefetch_l1(const uint32_t *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Warp-cooperative merge-path intersection of two single-segment sorted
 // leaf lists (both positive, one column each): tiles of 32 values from both
 // lists are loaded coalesced, each lane locates its A value in the B tile
@@ -488,6 +492,17 @@ __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const View &S
         const bool va = ia + l < ea, vb = ib + l < eb;
         const uint32_t av = va ? __ldg(ca + ia + l) : 0xffffffffu;
         const uint32_t bv = vb ? __ldg(cb + ib + l) : 0xffffffffu;
+        // the next tiles of both lists into L1 while this one is matched:
+        // every step consumes a full tile of at least one list, so the
+        // step after waits on an L1 hit instead of an L2 round trip
+        // (a 32-value tile spans at most two 128-byte lines: lanes 0-3 touch
+        // the first and last word of both next tiles)
+        if (l < 4) {
+            const uint32_t *base = (l & 1) ? cb + ib : ca + ia;
+            const uint32_t end = (l & 1) ? eb - ib : ea - ia;
+            const uint32_t off = 32 + (l >> 1) * 31;
+            if (off < end) prefetch_l1(base + off);
+        }
         const uint32_t na_tile = min(32u, ea - ia), nb_tile = min(32u, eb - ib);
         const uint32_t alast = __shfl_sync(kFull, av, na_tile - 1);
         const uint32_t blast = __shfl_sync(kFull, bv, nb_tile - 1);

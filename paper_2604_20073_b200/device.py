@@ -269,11 +269,27 @@ def jit_wait():
     lib().srdl_wcoj_jit_wait()
 
 
+_DEVICES: dict = {}
+_get_device = getattr(torch._C, "_cuda_getDevice", None)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def device() -> torch.device:
-    return torch.device("cuda", torch.cuda.current_device())
+    """The current CUDA device (cached torch.device per index: the engine
+    asks for it on every buffer allocation)."""
+    i = _get_device() if _get_device is not None else torch.cuda.current_device()
+    d = _DEVICES.get(i)
+    if d is None:
+        d = _DEVICES[i] = torch.device("cuda", i)
+    return d
 
 
 def stream_handle() -> int:
+    """cudaStream_t of torch's current stream on the current device (the raw
+    accessor: torch.cuda.current_stream() builds a Stream object per call,
+    a measurable cost at thousands of library calls per fixpoint)."""
+    if _raw_stream is not None and _get_device is not None:
+        return _raw_stream(_get_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -317,6 +333,23 @@ def sm_count() -> int:
 
 
 # ---------------------------------------------------------------- buffers
+
+
+def carve(*parts):
+    """Several device buffers from ONE allocation: parts are (n, dtype)
+    pairs; returns one tensor view per part (each 256-byte aligned). The
+    engine allocates a few buffers per library call thousands of times per
+    fixpoint; one allocation per call instead of several is a measurable
+    share of the host time per iteration (tools/host_profile.py)."""
+    offs, total = [], 0
+    for n, dt in parts:
+        offs.append(total)
+        total += -(-max(int(n), 0) * _ITEMSIZE[dt] // 256) * 256
+    buf = torch.empty(max(total, 256), dtype=torch.uint8, device=device())
+    return [buf[o:o + int(n) * _ITEMSIZE[dt]].view(dt) for o, (n, dt) in zip(offs, parts)]
+
+
+_ITEMSIZE = {torch.uint32: 4, torch.int32: 4, torch.int64: 8, torch.uint8: 1}
 
 
 def empty_rows(arity: int, n: int = 0) -> torch.Tensor:
@@ -422,13 +455,7 @@ def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Te
     """histogram_union with capacity-sized outputs; (K_delta, K_union) are
     written to k_slots[0:2] (uint32 device tensor) without a round trip."""
     n, nf = col.numel(), fkeys.numel()
-    d = device()
-    dk = torch.empty(n, dtype=U32, device=d)
-    dd = torch.empty(n, dtype=U32, device=d)
-    dp = torch.empty(n, dtype=U64, device=d)
-    uk = torch.empty(n + nf, dtype=U32, device=d)
-    ud = torch.empty(n + nf, dtype=U32, device=d)
-    up = torch.empty(n + nf, dtype=U64, device=d)
+    dk, dd, dp, uk, ud, up = carve((n, U32), (n, U32), (n, U64), (n + nf, U32), (n + nf, U32), (n + nf, U64))
     # algorithmic: the delta column, the full histogram (keys + degrees) read
     # once, both histograms written (key, degree, prefix: 16 B per key; sized
     # here by their upper bounds n and n + nf)
@@ -579,11 +606,9 @@ def root_work(okeys, odeg, oprefix=None, ikeys=None, ideg=None, iprefix=None, ou
     outer_lo / inner_lo (u32 first row of every key) are produced only when
     requested (single-segment sources); else None."""
     nk = okeys.numel()
-    d = device()
-    d2 = torch.empty(nk, dtype=U32, device=d)
-    prefix = torch.empty(nk, dtype=U64, device=d)
-    olo = torch.empty(nk, dtype=U32, device=d) if outer_rows else None
-    ilo = torch.empty(nk, dtype=U32, device=d) if inner_rows else None
+    d2, prefix, olo, ilo = carve((nk, U32), (nk, U64), (nk if outer_rows else 0, U32), (nk if inner_rows else 0, U32))
+    olo = olo if outer_rows else None
+    ilo = ilo if inner_rows else None
     if nk == 0:
         return d2, prefix, olo, ilo
     has_inner = ikeys is not None

@@ -166,10 +166,26 @@ def encode_shape(plan: JoinPlan, head_resolved=None) -> dev.PlanDesc:
     return d
 
 
+_SHAPES: dict = {}  # id(plan) -> (plan, head_resolved, shape descriptor)
+
+
+def _shape_template(plan: JoinPlan, head_resolved) -> dev.PlanDesc:
+    """encode_shape, memoised per plan object and head constants: the shape
+    is fixed for the life of a compiled program, while the descriptor is
+    rebuilt for every plan execution (every iteration)."""
+    hit = _SHAPES.get(id(plan))
+    if hit is None or hit[0] is not plan or hit[1] != head_resolved:
+        if len(_SHAPES) > 4096:
+            _SHAPES.clear()
+        hit = _SHAPES[id(plan)] = (plan, head_resolved, encode_shape(plan, head_resolved))
+    return hit[2]
+
+
 def encode_plan(prep: Prepared) -> dev.PlanDesc:
     """JoinPlan + resolved segments -> the fixed-size srdl_plan descriptor."""
     plan = prep.plan
-    d = encode_shape(plan, prep.head_resolved)
+    d = dev.PlanDesc()
+    C.pointer(d)[0] = _shape_template(plan, prep.head_resolved)  # copy of the shape fields
     for a, pa in enumerate(plan.atoms):
         ad = d.atom[a]
         src = prep.segs[a]
@@ -395,9 +411,9 @@ class SpecArena:
             storage = torch.empty(max(self.nchunks * per_chunk, 1), dtype=dev.U32, device=d)
         self.cols = storage[:arity * words].view(arity, words)
         self.chunk_next = storage[arity * words:arity * words + max(self.nchunks, 1)]
-        self.slice_first = torch.empty(nslices, dtype=dev.U32, device=d)
-        self.slice_spill = torch.empty(nslices, dtype=dev.U32, device=d)
-        self.meta = torch.empty(2, dtype=torch.int64, device=d)  # [spills, cursor]
+        # [spills, cursor], per-slice first chunk and spill flag: one allocation
+        self.meta, self.slice_first, self.slice_spill = dev.carve((2, torch.int64), (nslices, dev.U32),
+                                                                  (nslices, dev.U32))
         self._desc = None
 
     @property
@@ -433,13 +449,9 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec
         return CountResult.constant(n, 1 if prep.ok else 0)
     if not prep.ok or partition.nkeys == 0:
         return CountResult.constant(n, 0)
-    d = dev.device()
-    counts = CountResult(
-        torch.empty(n, dtype=dev.U64, device=d),
-        torch.empty(n, dtype=dev.U64, device=d),
-        torch.empty(1, dtype=dev.U64, device=d),
-        torch.empty(1, dtype=torch.int32, device=d),  # ticket: zeroed by srdl_wcoj_count
-    )
+    # per-slice counts and offsets, the total, the slice ticket (zeroed by
+    # srdl_wcoj_count): one allocation
+    counts = CountResult(*dev.carve((n, dev.U64), (n, dev.U64), (1, dev.U64), (1, torch.int32)))
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
     algo = input_bytes(prep) if dev.PROFILE is not None else 0

@@ -4,10 +4,13 @@ iteration.
 
     python tools/host_profile.py --workload doop [--top 40]
 """
-import argparse
+import os
+
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")  # as bench.py
+
+import argparse  # noqa: E402
 import cProfile
 import io
-import os
 import pstats
 import sys
 import time
