@@ -74,6 +74,16 @@ uint64_t srdl_launch_count(void);
 int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits,
                     uint32_t *const *out, uint64_t *n_out, void *stream);
 
+/* reference: RelationState.take_delta (storage.py:373-380), the delta of
+ * one iteration re-sorted under another index order. The rows are distinct
+ * and sorted by an order whose restriction to columns nkey.. of the target
+ * order (cols[] is given in TARGET order) is already their relative order,
+ * so one STABLE sort on the first nkey target columns finishes the job:
+ * nkey * bits key bits instead of arity * bits (e.g. (h, v) -> (v, h) sorts
+ * on v alone). out: `arity` arrays of n rows, target order. */
+int srdl_sort_reorder(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits, uint32_t nkey,
+                      uint32_t *const *out, void *stream);
+
 /* reference: storage.compute_delta (storage.py:311): distinct staged rows
  * minus the rows of up to eight sorted, duplicate-free segments (the full
  * relation's head and body, plus deltas of earlier chunks when a staging

@@ -172,8 +172,8 @@ void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t 
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *total_dev,
                         cudaStream_t s);
 void inclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, cudaStream_t s);
-// stable radix sort of keys (and optional 32-bit values) on the low `bits`
-// bits; results land back in keys/vals.
+// stable radix sort of keys (and optional 32-bit values) on key bits
+// [lo_bit, lo_bit + bits); results land back in keys/vals.
 void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s,
-                const int *unsorted = nullptr);
+                const int *unsorted = nullptr, uint32_t lo_bit = 0);
 }  // namespace srdl

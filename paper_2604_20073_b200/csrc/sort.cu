@@ -34,8 +34,8 @@ __device__ __forceinline__ uint64_t tile_index(uint64_t tile, int w, int r, int 
 
 // ghist[p * kBins + d] += number of keys whose pass-p digit is d
 __global__ void __launch_bounds__(kThreads)
-    radix_hist_all(const uint64_t *__restrict__ keys, uint64_t n, int passes, uint32_t *__restrict__ ghist,
-                   const int *__restrict__ unsorted) {
+    radix_hist_all(const uint64_t *__restrict__ keys, uint64_t n, int passes, int lo_bit,
+                   uint32_t *__restrict__ ghist, const int *__restrict__ unsorted) {
     if (unsorted && *unsorted == 0) return;  // input already in order: the sort is skipped
     __shared__ uint32_t h[kMaxPasses][kBins];
     for (int i = threadIdx.x; i < kMaxPasses * kBins; i += kThreads) (&h[0][0])[i] = 0;
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads)
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = __ldcs(keys + i);
-        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (p * kRadixBits)) & (kBins - 1)], 1u);
+        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (lo_bit + p * kRadixBits)) & (kBins - 1)], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) {
@@ -221,7 +221,7 @@ __global__ void copy_if_unsorted(T *__restrict__ dst, const T *__restrict__ src,
 // once and the keys stay in place, so a caller can skip sorting already
 // ordered input without a host round trip.
 void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaStream_t s,
-                const int *unsorted) {
+                const int *unsorted, uint32_t lo_bit) {
     if (n <= 1 || bits == 0) return;
     SRDL_REQUIRE(n < (1ull << 32), "radix_sort: %llu rows exceeds the 32-bit rank space",
                  (unsigned long long)n);
@@ -248,14 +248,15 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
     uint32_t *hist = meta.as<uint32_t>();
     uint32_t *tickets = hist + kMaxPasses * kBins;
     SRDL_CUDA(cudaMemsetAsync(hist, 0, hist_bytes + ticket_bytes, s));
-    radix_hist_all<<<stride_grid(n), kThreads, 0, s>>>(keys, n, passes, hist, unsorted);
+    SRDL_REQUIRE(lo_bit + bits <= 64, "radix_sort: bits [%u, %u) outside the key", lo_bit, lo_bit + bits);
+    radix_hist_all<<<stride_grid(n), kThreads, 0, s>>>(keys, n, passes, (int)lo_bit, hist, unsorted);
     SRDL_CHECK_LAUNCH();
     radix_digit_starts<<<1, 32 * kMaxPasses, 0, s>>>(hist, passes, unsorted);
     SRDL_CHECK_LAUNCH();
     uint64_t *kin = keys, *kout = kalt.as<uint64_t>();
     uint32_t *vin = vals, *vout = vals ? valt.as<uint32_t>() : nullptr;
     for (int p = 0; p < passes; ++p) {
-        const int shift = p * kRadixBits;
+        const int shift = (int)lo_bit + p * kRadixBits;
         SRDL_CUDA(cudaMemsetAsync(status.as<uint64_t>(), 0, status_bytes, s));
         if (vals)
             onesweep_pass<true><<<(unsigned)tiles, kThreads, onesweep_smem<true>(), s>>>(
@@ -439,6 +440,20 @@ __global__ void gather_cols(Cols cols, uint32_t arity, const uint32_t *__restric
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t r = idx[i];
         for (uint32_t c = 0; c < arity; ++c) out.c[c][i] = __ldg(cols.c[c] + r);
+    }
+}
+
+// every packed key back to `arity` columns of `bits` bits (no dedup)
+__global__ void unpack_all(const uint64_t *__restrict__ keys, uint64_t n, uint32_t arity, uint32_t bits,
+                           MutCols out) {
+    const uint64_t mask = bits >= 32 ? 0xffffffffull : ((1ull << bits) - 1);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        for (int c = (int)arity - 1; c >= 0; --c) {
+            out.c[c][i] = (uint32_t)(k & mask);
+            k >>= bits;
+        }
     }
 }
 
@@ -626,6 +641,42 @@ int srdl_compute_delta_async(const uint32_t *const *cols, uint32_t arity, uint64
             S.nseg++;
         }
         sort_unique_minus(cols, arity, n, bits, S, out, s, false, count_dev);
+    });
+}
+
+int srdl_sort_reorder(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits, uint32_t nkey,
+                      uint32_t *const *out, void *stream) {
+    return guarded([&] {
+        SRDL_REQUIRE(arity >= 1 && arity <= SRDL_MAX_COLS, "arity %u outside [1, %d]", arity, SRDL_MAX_COLS);
+        SRDL_REQUIRE(nkey >= 1 && nkey <= arity && bits >= 1 && bits <= 32 && nkey * bits <= 64,
+                     "sort_reorder: %u key columns of %u bits", nkey, bits);
+        if (n == 0) return;
+        SRDL_REQUIRE(n < (1ull << 32), "sort: %llu rows exceeds 2^32", (unsigned long long)n);
+        cudaStream_t s = (cudaStream_t)stream;
+        const Cols in = make_cols(cols, arity);
+        const MutCols dst = make_mut(out, arity);
+        const unsigned g = stride_grid(n);
+        Scratch keys(n * sizeof(uint64_t), s);
+        if (arity == 2 && nkey == 1) {
+            // both columns ride in one key (column 0 in the high word); only
+            // the high word's significant bits are sorted, stably
+            pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, 2}, 32, nullptr, n, keys.as<uint64_t>());
+            SRDL_CHECK_LAUNCH();
+            radix_sort(keys.as<uint64_t>(), nullptr, n, bits, s, nullptr, 32);
+            unpack_all<<<g, kThreads, 0, s>>>(keys.as<uint64_t>(), n, 2, 32, dst);
+            SRDL_CHECK_LAUNCH();
+            return;
+        }
+        // key columns packed, a stable sort carries the row permutation, all
+        // columns gathered through it
+        Scratch perm(n * sizeof(uint32_t), s);
+        pack_keys<<<g, kThreads, 0, s>>>(in, Chunk{0, nkey}, bits, nullptr, n, keys.as<uint64_t>());
+        SRDL_CHECK_LAUNCH();
+        iota_u32<<<g, kThreads, 0, s>>>(perm.as<uint32_t>(), n);
+        SRDL_CHECK_LAUNCH();
+        radix_sort(keys.as<uint64_t>(), perm.as<uint32_t>(), n, nkey * bits, s);
+        gather_cols<<<g, kThreads, 0, s>>>(in, arity, perm.as<uint32_t>(), n, dst);
+        SRDL_CHECK_LAUNCH();
     });
 }
 

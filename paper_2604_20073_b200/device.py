@@ -127,6 +127,9 @@ _SIGNATURES = {
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
     ),
+    "srdl_sort_reorder": (
+        C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]
+    ),
     "srdl_compute_delta": (
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -409,6 +412,38 @@ def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None, distinct: bool = 
     return out if distinct else _trim(out, got.value)
 
 
+def reorder_key_columns(order) -> int:
+    """For rows sorted in attribute order, the number of leading columns of
+    `order` a stable sort must key on so that the rows end up sorted in
+    `order`: the smallest P whose remaining columns order[P:] keep their
+    attribute order (0 = already in order)."""
+    order = list(order)
+    for p in range(len(order) + 1):
+        if order[p:] == sorted(order[p:]):
+            return p
+    return len(order)
+
+
+def sort_reorder(rows: torch.Tensor, bits: int, order) -> torch.Tensor:
+    """Distinct rows sorted in attribute order, re-sorted under `order` with
+    one stable sort on its leading columns (srdl_sort_reorder); falls back
+    to the full sort when those columns do not fit a 64-bit key."""
+    arity, n = rows.shape
+    order = list(order)
+    nkey = reorder_key_columns(order)
+    if nkey == 0:
+        return rows
+    if nkey * bits > 64:
+        return sort_dedup(rows, bits, order=order, distinct=True)
+    out = empty_rows(arity, n)
+    if n == 0:
+        return out
+    rc, _ = timed("sort_dedup", 8 * arity * n, lambda: lib().srdl_sort_reorder(
+        col_ptrs(rows, order), arity, n, bits, nkey, col_ptrs(out), stream_handle()))
+    check(rc, "sort_reorder")
+    return out
+
+
 def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:
     """sort_dedup(rows) minus the rows of the given sorted segments."""
     arity, n = rows.shape
@@ -451,11 +486,37 @@ def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: tor
     return out, rec
 
 
-def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor, k_slots: torch.Tensor):
+class BufferPool:
+    """Reusable device buffers for per-iteration outputs whose capacity is
+    known before their size: `get(key, parts)` returns views (as `carve`)
+    into a buffer kept under `key` and grown by 1.5x when too small. The
+    caller guarantees that the previous contents of a key are dead when it
+    asks again (ping-pong keys for outputs that must survive one iteration).
+    Per-iteration capacity allocations of 10-100 MB each were the largest
+    host cost of an iteration (tools/host_profile.py: torch.empty)."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key, *parts):
+        offs, total = [], 0
+        for n, dt in parts:
+            offs.append(total)
+            total += -(-max(int(n), 0) * _ITEMSIZE[dt] // 256) * 256
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < total:
+            buf = self.bufs[key] = torch.empty(max(int(total * 1.5), 256), dtype=torch.uint8, device=device())
+        return [buf[o:o + int(n) * _ITEMSIZE[dt]].view(dt) for o, (n, dt) in zip(offs, parts)]
+
+
+def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor, k_slots: torch.Tensor,
+                          pool: BufferPool | None = None, key=None):
     """histogram_union with capacity-sized outputs; (K_delta, K_union) are
-    written to k_slots[0:2] (uint32 device tensor) without a round trip."""
+    written to k_slots[0:2] (uint32 device tensor) without a round trip.
+    pool/key: take the outputs from a BufferPool instead of allocating."""
     n, nf = col.numel(), fkeys.numel()
-    dk, dd, dp, uk, ud, up = carve((n, U32), (n, U32), (n, U64), (n + nf, U32), (n + nf, U32), (n + nf, U64))
+    parts = ((n, U32), (n, U32), (n, U64), (n + nf, U32), (n + nf, U32), (n + nf, U64))
+    dk, dd, dp, uk, ud, up = pool.get(key, *parts) if pool is not None else carve(*parts)
     # algorithmic: the delta column, the full histogram (keys + degrees) read
     # once, both histograms written (key, degree, prefix: 16 B per key; sized
     # here by their upper bounds n and n + nf)

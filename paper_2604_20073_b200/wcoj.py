@@ -398,9 +398,11 @@ class SpecArena:
 
     __slots__ = ("cols", "chunk_next", "slice_first", "slice_spill", "meta", "nchunks", "_desc")
 
-    def __init__(self, arity: int, capacity: int, nslices: int, storage: torch.Tensor | None = None):
+    def __init__(self, arity: int, capacity: int, nslices: int, storage: torch.Tensor | None = None,
+                 pool=None, key=None):
         """storage: a uint32 device region to carve the tuple columns and
-        chunk links from (the engine's persistent arena), else allocated."""
+        chunk links from (the engine's persistent arena), else allocated;
+        pool/key: a dev.BufferPool slot for the per-slice bookkeeping."""
         d = dev.device()
         per_chunk = SPEC_CHUNK * arity + 1  # tuple columns + one link word
         if storage is not None:
@@ -412,8 +414,9 @@ class SpecArena:
         self.cols = storage[:arity * words].view(arity, words)
         self.chunk_next = storage[arity * words:arity * words + max(self.nchunks, 1)]
         # [spills, cursor], per-slice first chunk and spill flag: one allocation
-        self.meta, self.slice_first, self.slice_spill = dev.carve((2, torch.int64), (nslices, dev.U32),
-                                                                  (nslices, dev.U32))
+        parts = ((2, torch.int64), (nslices, dev.U32), (nslices, dev.U32))
+        self.meta, self.slice_first, self.slice_spill = (pool.get(key, *parts) if pool is not None
+                                                         else dev.carve(*parts))
         self._desc = None
 
     @property
@@ -437,7 +440,7 @@ class SpecArena:
 
 
 def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec_capacity=0,
-               spec_storage=None) -> CountResult:
+               spec_storage=None, buffers=None, key=None) -> CountResult:
     """Read-only pass: exact per-slice output counts, nothing written.
     spec_capacity > 0: the walk also writes its tuples speculatively into an
     arena of that many tuples (srdl_wcoj_count_spec); materialize_pass then
@@ -451,12 +454,14 @@ def count_pass(plan, store, partition, prep=None, interner=None, pool=None, spec
         return CountResult.constant(n, 0)
     # per-slice counts and offsets, the total, the slice ticket (zeroed by
     # srdl_wcoj_count): one allocation
-    counts = CountResult(*dev.carve((n, dev.U64), (n, dev.U64), (1, dev.U64), (1, torch.int32)))
+    parts = ((n, dev.U64), (n, dev.U64), (1, dev.U64), (1, torch.int32))
+    counts = CountResult(*(buffers.get(("count", key), *parts) if buffers is not None else dev.carve(*parts)))
     desc = prep.descriptor()
     x = _exec_desc(partition, counts)
     algo = input_bytes(prep) if dev.PROFILE is not None else 0
     if spec_capacity >= SPEC_CHUNK:
-        counts.spec = SpecArena(plan.head_arity, spec_capacity, n, spec_storage)
+        counts.spec = SpecArena(plan.head_arity, spec_capacity, n, spec_storage, buffers,
+                                ("spec", key) if buffers is not None else None)
         q = counts.spec.descriptor()
         rc, counts.event = _timed("wcoj_count", lambda: dev.lib().srdl_wcoj_count_spec(
             C.byref(desc), C.byref(x), C.byref(q), dev.stream_handle()), algo)
@@ -552,9 +557,11 @@ class PlanExecution:
             return True
         return bool(self.prep.ok) and self.partition.nkeys > 0
 
-    def count(self, spec_capacity: int = 0, spec_storage=None) -> CountResult:
+    def count(self, spec_capacity: int = 0, spec_storage=None, buffers=None, key=None) -> CountResult:
+        """buffers/key: a dev.BufferPool slot for the per-slice arrays (the
+        stream schedule reuses one per stream slot across iterations)."""
         self.counts = count_pass(self.plan, self.store, self.partition, self.prep, spec_capacity=spec_capacity,
-                                 spec_storage=spec_storage)
+                                 spec_storage=spec_storage, buffers=buffers, key=key)
         return self.counts
 
     def allocate(self, out=None):

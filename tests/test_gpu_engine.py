@@ -296,6 +296,13 @@ def test_batched_and_synchronous_delta_paths_agree(program):
         summary = engine.solve()
         results.append(({r: engine.relation_columns(r).cpu().numpy() for r in engine.compiled.declarations},
                         summary.rounds_by_rules()))
+        if stats is not None:
+            # the stream schedule records every join phase per plan, as the
+            # reference does (runtime.py:225-257)
+            plan_ids = {p.plan_id for st in engine.compiled.strata for p in st.plans}
+            rows = [r for r in stats.records if r["phase"] in ("histogram", "count", "materialize")]
+            assert rows and all(r["rule"] in plan_ids for r in rows)
+            assert {r["phase"] for r in rows} == {"histogram", "count", "materialize"}
     (a, ra), (b, rb) = results
     assert ra == rb
     for r in a:

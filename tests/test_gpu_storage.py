@@ -219,3 +219,18 @@ def test_sort_paths_device_and_host_branch(dev, arity, bits, layout, n):
         rs = dev.sort_dedup(got, bits, order=order, distinct=True)
         ref = want[:, order]
         assert np.array_equal(host(rs), ref[np.lexsort(ref.T[::-1])])
+
+
+@pytest.mark.parametrize("arity,bits,n", [(2, 27, 2_000_000), (2, 9, 5_000), (3, 21, 1_000_000), (4, 12, 300_000)])
+def test_sort_reorder_equals_full_sort(dev, arity, bits, n):
+    """srdl_sort_reorder (one stable sort on the leading target columns of a
+    sorted delta) gives exactly the full sort under every column order."""
+    import itertools
+
+    rng = np.random.default_rng(arity * 100 + bits)
+    rows = np.unique(rng.integers(0, 1 << bits, size=(n, arity)), axis=0).T.astype(np.uint32)
+    t = torch.from_numpy(np.ascontiguousarray(rows)).to(dev.device())
+    for order in itertools.permutations(range(arity)):
+        got = dev.sort_reorder(t, bits, order)
+        want = dev.sort_dedup(t, bits, order=order, distinct=True)
+        assert torch.equal(got, want), order
