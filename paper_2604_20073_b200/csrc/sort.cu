@@ -40,10 +40,18 @@ __global__ void __launch_bounds__(kThreads)
     __shared__ uint32_t h[kMaxPasses][kBins];
     for (int i = threadIdx.x; i < kMaxPasses * kBins; i += kThreads) (&h[0][0])[i] = 0;
     __syncthreads();
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = __ldcs(keys + i);
-        for (int p = 0; p < passes; ++p) atomicAdd(&h[p][(k >> (lo_bit + p * kRadixBits)) & (kBins - 1)], 1u);
+    // four independent loads per thread and round (memory-level parallelism)
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < n; base += 4 * stride) {
+        uint64_t k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) k[u] = base + u * stride < n ? __ldcs(keys + base + u * stride) : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (base + u * stride >= n) break;
+            for (int p = 0; p < passes; ++p)
+                atomicAdd(&h[p][(k[u] >> (lo_bit + p * kRadixBits)) & (kBins - 1)], 1u);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kBins; i += kThreads) {
@@ -84,7 +92,7 @@ constexpr size_t onesweep_smem() {
 }
 
 template <bool HAS_VALS>
-__global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)
+__global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per thread
     onesweep_pass(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n, int shift,
                   const uint32_t *__restrict__ starts, uint64_t *status, uint32_t *tile_ticket,
                   uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
@@ -108,12 +116,19 @@ __global__ void __launch_bounds__(kThreads, HAS_VALS ? 2 : 3)
     uint32_t v[kItems];
     uint32_t rank[kItems];
     const uint32_t lt = (1u << l) - 1u;
+    // all of the thread's keys in flight at once (the ranking loop below
+    // serialises on shared memory; loading inside it left one global load
+    // outstanding per warp: 45 % of stall samples on the key's first use)
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t i = tile_index(tile, w, r, l);
+        k[r] = i < n ? __ldcs(keys + i) : 0;
+        if (HAS_VALS) v[r] = i < n ? __ldcs(vals + i) : 0;
+    }
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const uint64_t i = tile_index(tile, w, r, l);
         const bool ok = i < n;
-        k[r] = ok ? __ldcs(keys + i) : 0;
-        if (HAS_VALS) v[r] = ok ? __ldcs(vals + i) : 0;
         const uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t before = 0;
@@ -291,14 +306,31 @@ struct Chunk {
     uint32_t first, count;  // columns [first, first+count)
 };
 
+// Elementwise kernels below keep kIlp independent loads in flight per
+// thread (a grid-stride loop with one load per round is capped near 2-3 TB/s
+// by the ~300 K resident threads of the device, Little's law).
+constexpr int kIlp = 4;
+
 __global__ void pack_keys(Cols cols, Chunk ch, uint32_t bits, const uint32_t *__restrict__ perm,
                           uint64_t n, uint64_t *__restrict__ keys) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t row = perm ? perm[i] : i;
-        uint64_t k = 0;
-        for (uint32_t c = 0; c < ch.count; ++c) k = (k << bits) | __ldg(cols.c[ch.first + c] + row);
-        keys[i] = k;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < n; base += kIlp * stride) {
+        uint64_t row[kIlp], k[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const uint64_t i = base + u * stride;
+            row[u] = i < n ? (perm ? __ldg(perm + i) : i) : 0;
+            k[u] = 0;
+        }
+        for (uint32_t c = 0; c < ch.count; ++c) {
+            const uint32_t *col = cols.c[ch.first + c];
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u)
+                if (base + u * stride < n) k[u] = (k[u] << bits) | __ldg(col + row[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u)
+            if (base + u * stride < n) keys[base + u * stride] = k[u];
     }
 }
 
@@ -327,23 +359,44 @@ struct Segs {
 // keep[i] = first of its run of equal keys (membership in the full
 // segments is removed afterwards by the merge-path anti-join)
 __global__ void flag_keys(const uint64_t *__restrict__ keys, uint64_t n, uint32_t *__restrict__ keep) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        keep[i] = (i == 0) || keys[i - 1] != keys[i];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < n; base += kIlp * stride) {
+        uint64_t a[kIlp], b[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const uint64_t i = base + u * stride;
+            b[u] = i < n ? __ldg(keys + i) : 0;
+            a[u] = i < n && i > 0 ? __ldg(keys + i - 1) : ~b[u];
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u)
+            if (base + u * stride < n) keep[base + u * stride] = a[u] != b[u];
+    }
 }
 
 __global__ void scatter_unpack(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ keep,
                                const uint32_t *__restrict__ pos, uint64_t n, uint32_t arity,
                                uint32_t bits, MutCols out) {
     const uint64_t mask = bits >= 32 ? 0xffffffffull : ((1ull << bits) - 1);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if (!keep[i]) continue;
-        uint64_t k = keys[i];
-        uint32_t p = pos[i];
-        for (int c = (int)arity - 1; c >= 0; --c) {
-            out.c[c][p] = (uint32_t)(k & mask);
-            k >>= bits;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t base = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; base < n; base += kIlp * stride) {
+        uint32_t kp[kIlp], p[kIlp];
+        uint64_t k[kIlp];
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            const uint64_t i = base + u * stride;
+            kp[u] = i < n ? __ldg(keep + i) : 0;
+            k[u] = i < n ? __ldg(keys + i) : 0;
+            p[u] = i < n ? __ldg(pos + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kIlp; ++u) {
+            if (!kp[u]) continue;
+            uint64_t x = k[u];
+            for (int c = (int)arity - 1; c >= 0; --c) {
+                out.c[c][p[u]] = (uint32_t)(x & mask);
+                x >>= bits;
+            }
         }
     }
 }

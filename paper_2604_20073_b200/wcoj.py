@@ -229,6 +229,16 @@ def jit_prepare(plans, mode="spec", wait=False) -> int:
     return dev.lib().srdl_wcoj_jit_prepare(arr, len(plans), KERNEL_MODES[mode], int(wait))
 
 
+def emits_sorted_distinct(plan: JoinPlan) -> bool:
+    """The plan's output, in emission order, is strictly increasing: its head
+    is every variable in level order (one row per binding, so distinct) and
+    the walk enumerates bindings lexicographically — slices are contiguous
+    in root-key order, rectangles row-major, candidates and leaf batches in
+    row order, merge-path parents in lane order (csrc/wcoj_kernel.cuh)."""
+    return bool(plan.depth) and plan.head_arity == plan.depth and all(
+        kind == VAR and x == h for h, (kind, x) in enumerate(plan.head_cols))
+
+
 def hist_covers(rel, rows) -> bool:
     """The index histogram describes exactly `rows` (its only segment)."""
     return rel.size == rows.shape[1]
