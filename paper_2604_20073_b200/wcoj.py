@@ -239,6 +239,14 @@ def emits_sorted_distinct(plan: JoinPlan) -> bool:
         kind == VAR and x == h for h, (kind, x) in enumerate(plan.head_cols))
 
 
+def execution_sorted(prep: "Prepared") -> bool:
+    """This execution of the plan emits strictly increasing rows: the plan
+    does (emits_sorted_distinct) and every source is ONE sorted segment — an
+    index with a head buffer is walked body first, then head, so a level's
+    candidates are then two sorted runs, not one."""
+    return emits_sorted_distinct(prep.plan) and all(len(src) <= 1 for src in prep.segs)
+
+
 def hist_covers(rel, rows) -> bool:
     """The index histogram describes exactly `rows` (its only segment)."""
     return rel.size == rows.shape[1]
