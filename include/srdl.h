@@ -322,6 +322,8 @@ int srdl_wcoj_materialize_spilled(const srdl_plan *plan, const srdl_exec *ex, co
 int srdl_wcoj_jit_prepare(const srdl_plan *plans, uint32_t n, int mode, int wait);
 /* Block until the background compiler is idle. */
 void srdl_wcoj_jit_wait(void);
+/* Drop queued compilations and wait for running ones (process exit). */
+void srdl_wcoj_jit_shutdown(void);
 /* 0 off, 1 async, 2 sync; returns the previous mode. */
 int srdl_wcoj_jit_set_mode(int mode);
 /* Generated source of a plan's kernel (truncated to cap bytes); returns its length. */

@@ -235,6 +235,142 @@ __global__ void write_zero(T *p) {
     *p = 0;
 }
 
+// Single-pass scan (chained scan with decoupled look-back, Merrill &
+// Garland): tile t scans its 4096 elements, publishes its aggregate, warp 0
+// looks back over the preceding tiles' published aggregates / inclusive
+// prefixes 32 at a time, and the tile writes its outputs — one launch
+// instead of reduce + scan-of-partials + scan. The status words carry a
+// per-call epoch, so the persistent status buffer (per device / stream /
+// thread) is never cleared: a stale word from an earlier call has a smaller
+// epoch and reads as "not published".
+constexpr uint64_t kStAgg = 1, kStInc = 2;
+
+template <class T>
+__device__ __forceinline__ T wsum_total(const T *wsum) {
+    T t = 0;
+    for (int k = 0; k < kWarps; ++k) t += wsum[k];
+    return t;
+}
+
+template <class T, bool EXCLUSIVE>
+__global__ void __launch_bounds__(kThreads)
+    chained_scan(const T *__restrict__ in, T *__restrict__ out, uint64_t n, T *__restrict__ total,
+                 uint64_t *status, uint64_t *value, uint64_t epoch) {
+    __shared__ T wsum[kWarps];
+    __shared__ T wbase[kWarps];
+    __shared__ uint64_t tile_excl;
+    const uint64_t tile = blockIdx.x;  // blocks are dispatched in index order
+    const uint64_t base = tile * kTile;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    T x[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
+        x[r] = i < n ? in[i] : T(0);
+    }
+    T v[kItems];
+    T carry = 0;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        T s = x[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, s, o);
+            if (l >= o) s += y;
+        }
+        v[r] = carry + (EXCLUSIVE ? s - x[r] : s);
+        carry += __shfl_sync(0xffffffffu, s, 31);
+    }
+    if (l == 0) wsum[w] = carry;
+    __syncthreads();
+    if (w == 0) {
+        T agg = 0;
+        if (l == 0) {
+            T run = 0;
+            for (int k = 0; k < kWarps; ++k) {
+                wbase[k] = run;
+                run += wsum[k];
+            }
+            agg = run;
+            value[tile] = (uint64_t)run;
+            __threadfence();
+            *(volatile uint64_t *)(status + tile) = (epoch << 2) | (tile == 0 ? kStInc : kStAgg);
+        }
+        agg = __shfl_sync(0xffffffffu, agg, 0);
+        uint64_t excl = 0;
+        if (tile > 0) {
+            // look back 32 tiles at a time: lane j inspects tile t - j
+            int64_t t = (int64_t)tile - 1;
+            while (true) {
+                const int64_t mine = t - l;
+                uint64_t st = 0, val = 0;
+                if (mine >= 0) {
+                    do {
+                        st = *(volatile uint64_t *)(status + mine);
+                    } while ((st >> 2) != epoch);
+                    __threadfence();
+                    val = *(volatile uint64_t *)(value + mine);
+                } else {
+                    st = (epoch << 2) | kStInc;  // before tile 0: empty inclusive prefix
+                }
+                const uint32_t inc = __ballot_sync(0xffffffffu, (st & 3) == kStInc);
+                const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive tile
+                uint64_t part = l <= first ? val : 0;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                excl += part;
+                if (inc) break;
+                t -= 32;
+            }
+            if (l == 0) {
+                value[tile] = excl + (uint64_t)agg;
+                __threadfence();
+                *(volatile uint64_t *)(status + tile) = (epoch << 2) | kStInc;
+            }
+        }
+        if (l == 0) tile_excl = excl;
+    }
+    __syncthreads();
+    const T add = wbase[w] + (T)tile_excl;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
+        if (i < n) out[i] = v[r] + add;
+    }
+    if (total && tile == gridDim.x - 1 && threadIdx.x == 0) *total = (T)(tile_excl + wsum_total(wsum));
+}
+
+namespace {
+
+// persistent look-back status of one (device, stream, thread): grown, never cleared
+struct ScanState {
+    uint64_t *status = nullptr, *value = nullptr;
+    size_t cap = 0;
+    uint64_t epoch = 0;
+};
+
+std::mutex g_scan_mu;
+std::unordered_map<ArenaKey, ScanState, ArenaKeyHash> g_scan;
+
+ScanState &scan_state(cudaStream_t s, size_t tiles) {
+    const ArenaKey key = arena_key(s);
+    std::lock_guard<std::mutex> lock(g_scan_mu);
+    ScanState &st = g_scan[key];
+    if (st.cap < tiles) {
+        // the old buffers may still be read by queued scans of this stream:
+        // they are leaked rather than freed (a few growth steps per process)
+        size_t cap = st.cap ? st.cap : 1024;
+        while (cap < tiles) cap *= 2;
+        SRDL_CUDA(cudaMalloc(&st.status, cap * sizeof(uint64_t)));
+        SRDL_CUDA(cudaMalloc(&st.value, cap * sizeof(uint64_t)));
+        SRDL_CUDA(cudaMemsetAsync(st.status, 0, cap * sizeof(uint64_t), s));  // epoch 0 = never published
+        st.cap = cap;
+    }
+    return st;
+}
+
+}  // namespace
+
 template <class T, bool EXCLUSIVE>
 static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s) {
     if (n == 0) {
@@ -250,11 +386,9 @@ static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s)
         SRDL_CHECK_LAUNCH();
         return;
     }
-    Scratch part(blocks * sizeof(T), s);
-    tile_reduce<T><<<(unsigned)blocks, kThreads, 0, s>>>(in, n, part.as<T>());
-    SRDL_CHECK_LAUNCH();
-    scan_impl<T, true>(part.as<T>(), part.as<T>(), blocks, nullptr, s);
-    tile_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, part.as<T>(), total);
+    ScanState &st = scan_state(s, blocks);
+    const uint64_t epoch = ++st.epoch;
+    chained_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, total, st.status, st.value, epoch);
     SRDL_CHECK_LAUNCH();
 }
 

@@ -85,6 +85,20 @@ constexpr uint64_t kFlagAgg = 1ull << 62;  // this tile's own count is published
 constexpr uint64_t kFlagInc = 2ull << 62;  // inclusive prefix through this tile
 constexpr uint64_t kValMask = (1ull << 62) - 1;
 
+// Lanes of the warp holding the same digit as this lane (invalid lanes,
+// digit kBins, group among themselves): one ballot per digit bit instead of
+// __match_any_sync, which stalled the ranking loop (short_scoreboard 60 %).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool ok) {
+    uint32_t peers = __ballot_sync(0xffffffffu, ok);
+    if (!ok) peers = ~peers;
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
+    }
+    return peers;
+}
+
 template <bool HAS_VALS>
 constexpr size_t onesweep_smem() {
     return (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0) + (size_t)kWarps * kBins * 4 +
@@ -130,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
         const uint64_t i = tile_index(tile, w, r, l);
         const bool ok = i < n;
         const uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = digit_peers(d, ok);
         uint32_t before = 0;
         if (ok) before = cnt[w][d];
         __syncwarp();

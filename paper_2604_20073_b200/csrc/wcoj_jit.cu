@@ -474,6 +474,19 @@ void srdl_wcoj_jit_wait(void) {
     g_pool.idle.wait(lock, [] { return g_pool.queue.empty() && g_pool.busy == 0; });
 }
 
+// Drop the kernels still queued for the background compiler and wait for
+// the ones being compiled (process exit: no worker may outlive the CUDA
+// runtime and NVRTC).
+void srdl_wcoj_jit_shutdown(void) {
+    std::unique_lock<std::mutex> lock(g_pool.mu);
+    for (auto &e : g_pool.queue) {
+        std::lock_guard<std::mutex> el(e->mu);
+        e->state = 0;  // never built; a later request schedules it again
+    }
+    g_pool.queue.clear();
+    g_pool.idle.wait(lock, [] { return g_pool.busy == 0; });
+}
+
 // Set the per-plan kernel mode (0 off, 1 background, 2 compile on first
 // use); returns the previous mode. Default: SRDL_JIT (0 / async / sync).
 int srdl_wcoj_jit_set_mode(int mode) { return g_mode.exchange(mode); }

@@ -189,6 +189,7 @@ _SIGNATURES = {
     "srdl_wcoj_count": (C.c_int, [C.POINTER(PlanDesc), C.POINTER(ExecDesc), C.c_void_p]),
     "srdl_wcoj_jit_prepare": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int, C.c_int]),
     "srdl_wcoj_jit_wait": (None, []),
+    "srdl_wcoj_jit_shutdown": (None, []),
     "srdl_wcoj_jit_set_mode": (C.c_int, [C.c_int]),
     "srdl_wcoj_jit_source": (C.c_uint64, [C.c_void_p, C.c_int, C.c_char_p, C.c_uint64]),
     "srdl_wcoj_jit_compile_check": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_uint64)]),
@@ -246,6 +247,10 @@ def lib():
         _LIB = load_library()
         if _LIB.srdl_version() != 1:
             raise DeviceUnavailable("libsrdl.so version mismatch; rebuild it")
+        import atexit
+
+        # background kernel compiles must not outlive the interpreter
+        atexit.register(_LIB.srdl_wcoj_jit_shutdown)
     return _LIB
 
 
