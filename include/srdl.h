@@ -62,6 +62,10 @@ const char *srdl_last_error(void);
 int srdl_sm_count(void);
 /* Kernels launched by this library since load (process-wide counter). */
 uint64_t srdl_launch_count(void);
+/* Device-wide prefix sums (exclusive or inclusive; total = sum, exclusive
+ * only, device pointer or NULL). in and out may alias. */
+int srdl_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, int exclusive, uint32_t *total, void *stream);
+int srdl_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, int exclusive, uint64_t *total, void *stream);
 
 /* --------------------------------------------------------------- storage
  * reference: rowops.sort_dedup (rowops.py:60) / storage.sort_dedup
@@ -152,6 +156,11 @@ int srdl_histogram_union_async(const uint32_t *col, uint64_t n, const uint32_t *
  * off has n_ids + 1 entries. The CSR row index of a sorted relation. */
 int srdl_dense_offsets(const uint32_t *keys, const uint64_t *prefix, uint64_t nkeys,
                        uint32_t n_ids, uint32_t *off, void *stream);
+
+/* Largest id over `arity` columns of n rows into *max_dev (device memory;
+ * 0 for n == 0): the id space an engine reserves for integer EDB columns
+ * (reference: interning of integer constants, interning.py). */
+int srdl_max_id(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t *max_dev, void *stream);
 
 /* Fence keys of a sorted key array: fence[i] = keys[i * SRDL_FENCE] for
  * i < ceil(n / SRDL_FENCE) (the first level of the two-level column-0 search

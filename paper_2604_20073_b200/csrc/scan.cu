@@ -255,7 +255,7 @@ __device__ __forceinline__ T wsum_total(const T *wsum) {
 template <class T, bool EXCLUSIVE>
 __global__ void __launch_bounds__(kThreads)
     chained_scan(const T *__restrict__ in, T *__restrict__ out, uint64_t n, T *__restrict__ total,
-                 uint64_t *status, uint64_t *value, uint64_t epoch) {
+                 uint64_t *status, uint64_t *value, uint64_t cap, uint64_t epoch) {
     __shared__ T wsum[kWarps];
     __shared__ T wbase[kWarps];
     __shared__ uint64_t tile_excl;
@@ -292,7 +292,11 @@ __global__ void __launch_bounds__(kThreads)
                 run += wsum[k];
             }
             agg = run;
+            // aggregate and inclusive prefix live in separate words (value[t]
+            // and value[cap + t]): a reader that saw "aggregate" must not read
+            // a word the tile has meanwhile overwritten with its inclusive sum
             value[tile] = (uint64_t)run;
+            if (tile == 0) value[cap + tile] = (uint64_t)run;
             __threadfence();
             *(volatile uint64_t *)(status + tile) = (epoch << 2) | (tile == 0 ? kStInc : kStAgg);
         }
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(kThreads)
                         st = *(volatile uint64_t *)(status + mine);
                     } while ((st >> 2) != epoch);
                     __threadfence();
-                    val = *(volatile uint64_t *)(value + mine);
+                    val = *(volatile uint64_t *)(value + ((st & 3) == kStInc ? cap : 0) + mine);
                 } else {
                     st = (epoch << 2) | kStInc;  // before tile 0: empty inclusive prefix
                 }
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__(kThreads)
                 t -= 32;
             }
             if (l == 0) {
-                value[tile] = excl + (uint64_t)agg;
+                value[cap + tile] = excl + (uint64_t)agg;
                 __threadfence();
                 *(volatile uint64_t *)(status + tile) = (epoch << 2) | kStInc;
             }
@@ -362,7 +366,7 @@ ScanState &scan_state(cudaStream_t s, size_t tiles) {
         size_t cap = st.cap ? st.cap : 1024;
         while (cap < tiles) cap *= 2;
         SRDL_CUDA(cudaMalloc(&st.status, cap * sizeof(uint64_t)));
-        SRDL_CUDA(cudaMalloc(&st.value, cap * sizeof(uint64_t)));
+        SRDL_CUDA(cudaMalloc(&st.value, 2 * cap * sizeof(uint64_t)));  // aggregates, inclusive prefixes
         SRDL_CUDA(cudaMemsetAsync(st.status, 0, cap * sizeof(uint64_t), s));  // epoch 0 = never published
         st.cap = cap;
     }
@@ -388,7 +392,8 @@ static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s)
     }
     ScanState &st = scan_state(s, blocks);
     const uint64_t epoch = ++st.epoch;
-    chained_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, total, st.status, st.value, epoch);
+    chained_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, total, st.status, st.value, st.cap,
+                                                                       epoch);
     SRDL_CHECK_LAUNCH();
 }
 
@@ -409,6 +414,28 @@ void inclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, cudaStrea
 extern "C" {
 
 int srdl_version(void) { return SRDL_VERSION; }
+
+// Device-wide scans (the two-phase allocation's offsets, reference
+// executor.py:516-524 np.cumsum of the per-slice counts), exposed for tests.
+int srdl_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, int exclusive, uint32_t *total, void *stream) {
+    return srdl::guarded([&] {
+        SRDL_REQUIRE(exclusive || total == nullptr, "an inclusive scan has no separate total");
+        if (exclusive)
+            srdl::exclusive_scan_u32(in, out, n, total, (cudaStream_t)stream);
+        else
+            srdl::scan_impl<uint32_t, false>(in, out, n, nullptr, (cudaStream_t)stream);
+    });
+}
+
+int srdl_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, int exclusive, uint64_t *total, void *stream) {
+    return srdl::guarded([&] {
+        SRDL_REQUIRE(exclusive || total == nullptr, "an inclusive scan has no separate total");
+        if (exclusive)
+            srdl::exclusive_scan_u64(in, out, n, total, (cudaStream_t)stream);
+        else
+            srdl::inclusive_scan_u64(in, out, n, (cudaStream_t)stream);
+    });
+}
 
 uint64_t srdl_launch_count(void) { return srdl::launches(); }
 

@@ -346,6 +346,18 @@ static uint64_t histogram_impl(const uint32_t *col, uint64_t n, uint32_t *keys, 
     return K;
 }
 
+// max over the columns of a row set (atomicMax of per-warp maxima)
+__global__ void max_rows(Cols cols, uint32_t arity, uint64_t n, uint32_t *__restrict__ out) {
+    uint32_t m = 0;
+    for (uint32_t c = 0; c < arity; ++c)
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+             i += (uint64_t)gridDim.x * blockDim.x)
+            m = max(m, __ldg(cols.c[c] + i));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // ---- packed exchange buffers (multi-GPU all-to-all, dist.py)
 
 __global__ void owner_keys(const uint32_t *__restrict__ col, uint64_t n, uint32_t world,
@@ -539,6 +551,16 @@ static void histogram_union_impl(const uint32_t *col, uint64_t n, const uint32_t
 }
 
 extern "C" {
+
+int srdl_max_id(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t *max_dev, void *stream) {
+    return guarded([&] {
+        cudaStream_t s = (cudaStream_t)stream;
+        SRDL_CUDA(cudaMemsetAsync(max_dev, 0, sizeof(uint32_t), s));
+        if (n == 0) return;
+        max_rows<<<stride_grid(n), kThreads, 0, s>>>(make_cols(cols, arity), arity, n, max_dev);
+        SRDL_CHECK_LAUNCH();
+    });
+}
 
 int srdl_key_fence(const uint32_t *keys, uint64_t n, uint32_t *fence, void *stream) {
     return guarded([&] {

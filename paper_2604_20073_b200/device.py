@@ -123,6 +123,8 @@ _SIGNATURES = {
     "srdl_last_error": (C.c_char_p, []),
     "srdl_sm_count": (C.c_int, []),
     "srdl_launch_count": (C.c_uint64, []),
+    "srdl_scan_u32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
+    "srdl_scan_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
     "srdl_sort_dedup": (
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p],
@@ -172,6 +174,7 @@ _SIGNATURES = {
     "srdl_wcoj_count_spec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "srdl_wcoj_gather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "srdl_wcoj_materialize_spilled": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "srdl_max_id": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p]),
     "srdl_key_fence": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]),
     "srdl_dense_offsets": (
         C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]
@@ -630,6 +633,27 @@ def histogram_union(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Tensor):
 
 
 FENCE = 64  # SRDL_FENCE
+
+
+def max_ids(row_sets) -> list:
+    """Largest id of each uint32 row set, one kernel per set and ONE host
+    read for all of them."""
+    out = torch.zeros(max(len(row_sets), 1), dtype=torch.int32, device=device())
+    for i, rows in enumerate(row_sets):
+        check(lib().srdl_max_id(col_ptrs(rows) if rows.numel() else None, rows.shape[0], rows.shape[1],
+                                out[i:i + 1].data_ptr(), stream_handle()), "max_id")
+    return [int(v) & 0xFFFFFFFF for v in out.tolist()][:len(row_sets)]
+
+
+def scan(x: torch.Tensor, exclusive: bool = True):
+    """(prefix sums of a 1-D uint32 / int64 device tensor, total or None)."""
+    n = x.numel()
+    out = torch.empty_like(x)
+    total = torch.zeros(1, dtype=x.dtype, device=x.device) if exclusive else None
+    fn = lib().srdl_scan_u64 if x.element_size() == 8 else lib().srdl_scan_u32
+    check(fn(x.data_ptr() if n else None, out.data_ptr() if n else None, n, int(exclusive),
+             total.data_ptr() if total is not None else None, stream_handle()), "scan")
+    return out, total
 
 
 def key_fence(keys: torch.Tensor) -> torch.Tensor:

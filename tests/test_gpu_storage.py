@@ -234,3 +234,24 @@ def test_sort_reorder_equals_full_sort(dev, arity, bits, n):
         got = dev.sort_reorder(t, bits, order)
         want = dev.sort_dedup(t, bits, order=order, distinct=True)
         assert torch.equal(got, want), order
+
+
+@pytest.mark.parametrize("n", [1, 4096, 4097, 5000, 100_003, 3_000_001, 40_000_000])
+@pytest.mark.parametrize("wide", [False, True])
+def test_scans_match_cumsum(dev, n, wide):
+    """Single-pass chained scans (u32 / u64, exclusive with total, inclusive,
+    in place) against torch.cumsum, across one and many tiles."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randint(0, 7, (n,), device="cuda", generator=g, dtype=torch.int64)
+    ref = torch.cumsum(x, 0)
+    src = x if wide else x.to(torch.int32).view(torch.uint32)
+    out, total = dev.scan(src, exclusive=True)
+    got = out.view(torch.int64) if wide else out.view(torch.int32).to(torch.int64)
+    assert torch.equal(got, ref - x)
+    assert int(total.view(torch.int64 if wide else torch.int32)[0]) == int(ref[-1])
+    inc, _ = dev.scan(src, exclusive=False)
+    got = inc.view(torch.int64) if wide else inc.view(torch.int32).to(torch.int64)
+    assert torch.equal(got, ref)
+    for _ in range(3):  # repeated calls reuse the epoch-stamped status
+        out2, _ = dev.scan(src, exclusive=True)
+        assert torch.equal(out2, out)
