@@ -46,8 +46,10 @@ def family_of(kernel: str):
 def main():
     path, workload, bench_path = sys.argv[1], sys.argv[2], sys.argv[3]
     bench = json.loads(open(bench_path).read().strip().splitlines()[-1])
-    # fixpoints the bench ran: warm-up, timed, e2e (min(steps, 3)) and parity
-    fixpoints = bench["warmup"] + bench["steps"] + max(1, min(bench["steps"], 3)) + (1 if "parity" in bench else 0)
+    # fixpoints the bench ran: warm-up, timed, profiled, e2e (min(steps, 3)) and parity
+    rl0 = bench.get("roofline") or {}
+    fixpoints = (bench["warmup"] + bench["steps"] + rl0.get("profiled_steps", 0) + max(1, min(bench["steps"], 3))
+                 + (1 if "parity" in bench else 0))
     rl = bench.get("roofline") or {}
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
@@ -75,7 +77,7 @@ def main():
     for fam, (launches, b) in agg.items():
         calls = None
         if rl.get("kernel") == fam:
-            calls = rl["launches_per_step"] * fixpoints
+            calls = rl["launches_per_step"] * fixpoints  # per-step calls of the profiled steps
         rec[fam] = round(b / calls) if calls else None
         rec[fam + "_kernel_launches"] = launches
         rec[fam + "_bytes_total"] = round(b)
