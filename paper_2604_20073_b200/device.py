@@ -295,10 +295,48 @@ def device() -> torch.device:
     return d
 
 
+_LAUNCH = None  # (torch Stream, handle) while launch_on() is active
+
+
+class launch_on:
+    """Launch library calls on `stream` while buffers keep being allocated on
+    torch's current stream. The engine uses it for fork-join phases: the
+    main stream launches nothing between the fork (stream.wait_stream(main))
+    and the join (main.wait_stream(stream)), so memory freed by the host in
+    between is only reused by main-stream work ordered after the join."""
+
+    def __init__(self, stream):
+        self.stream = stream
+
+    def __enter__(self):
+        global _LAUNCH
+        self.prev = _LAUNCH
+        _LAUNCH = (self.stream, self.stream.cuda_stream)
+        return self
+
+    def __exit__(self, *exc):
+        global _LAUNCH
+        _LAUNCH = self.prev
+
+
+def _uses(*tensors):
+    """Inside launch_on(): the side stream reads these tensors, so the
+    caching allocator must not reuse their memory before that stream gets
+    past this point (a temporary the host drops right after the launch)."""
+    if _LAUNCH is not None:
+        s = _LAUNCH[0]
+        for t in tensors:
+            if t is not None and t.numel():
+                t.record_stream(s)
+
+
 def stream_handle() -> int:
-    """cudaStream_t of torch's current stream on the current device (the raw
-    accessor: torch.cuda.current_stream() builds a Stream object per call,
-    a measurable cost at thousands of library calls per fixpoint)."""
+    """cudaStream_t library calls launch on: the launch_on() stream, else
+    torch's current stream on the current device (the raw accessor:
+    torch.cuda.current_stream() builds a Stream object per call, a
+    measurable cost at thousands of library calls per fixpoint)."""
+    if _LAUNCH is not None:
+        return _LAUNCH[1]
     if _raw_stream is not None and _get_device is not None:
         return _raw_stream(_get_device())
     return torch.cuda.current_stream().cuda_stream
@@ -318,9 +356,10 @@ def timed(family: str, algo_bytes: int, fn):
         return fn(), None
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
-    a.record()
+    on = _LAUNCH[0] if _LAUNCH is not None else None
+    a.record(on)
     rc = fn()
-    b.record()
+    b.record(on)
     rec = [family, a, b, int(algo_bytes)]
     PROFILE.append(rec)
     return rc, rec
@@ -411,6 +450,7 @@ def sort_dedup(rows: torch.Tensor, bits: int = 32, order=None, distinct: bool = 
     if n == 0:
         return out
     got = C.c_uint64(0)
+    _uses(rows, out)
     rc, rec = timed("sort_dedup", 4 * arity * n, lambda: lib().srdl_sort_dedup(
         col_ptrs(rows, order), len(order), n, bits, col_ptrs(out), None if distinct else C.byref(got),
         stream_handle()))
@@ -446,6 +486,7 @@ def sort_reorder(rows: torch.Tensor, bits: int, order) -> torch.Tensor:
     out = empty_rows(arity, n)
     if n == 0:
         return out
+    _uses(rows, out)
     rc, _ = timed("sort_dedup", 8 * arity * n, lambda: lib().srdl_sort_reorder(
         col_ptrs(rows, order), arity, n, bits, nkey, col_ptrs(out), stream_handle()))
     check(rc, "sort_reorder")
@@ -487,6 +528,7 @@ def compute_delta_async(rows: torch.Tensor, segments, bits: int, count_slot: tor
     seg_ptr_arrays = [col_ptrs(s) for s in segs]
     seg_cols = (C.c_void_p * MAX_DIFF_SEGS)(*[C.addressof(a) for a in seg_ptr_arrays])
     seg_rows = (C.c_uint64 * MAX_DIFF_SEGS)(*[nrows(s) for s in segs])
+    _uses(rows, out, *segs)
     rc, rec = timed("compute_delta", 4 * arity * n, lambda: lib().srdl_compute_delta_async(
         col_ptrs(rows) if n else None, arity, n, bits, seg_cols, seg_rows, len(segs),
         col_ptrs(out) if n else None, count_slot.data_ptr(), stream_handle()))
@@ -525,6 +567,7 @@ def histogram_union_async(col: torch.Tensor, fkeys: torch.Tensor, fdeg: torch.Te
     n, nf = col.numel(), fkeys.numel()
     parts = ((n, U32), (n, U32), (n, U64), (n + nf, U32), (n + nf, U32), (n + nf, U64))
     dk, dd, dp, uk, ud, up = pool.get(key, *parts) if pool is not None else carve(*parts)
+    _uses(col, fkeys, fdeg, dk, uk)
     # algorithmic: the delta column, the full histogram (keys + degrees) read
     # once, both histograms written (key, degree, prefix: 16 B per key; sized
     # here by their upper bounds n and n + nf)
@@ -545,6 +588,7 @@ def merge(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     if na == 0:
         return b
     out = empty_rows(arity, na + nb)
+    _uses(a, b, out)
     rc, _ = timed("merge", 8 * arity * (na + nb), lambda: lib().srdl_merge(
         col_ptrs(a), na, col_ptrs(b), nb, arity, col_ptrs(out), stream_handle()))
     check(rc, "merge")
