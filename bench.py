@@ -229,6 +229,14 @@ def profile_traffic(workload_name, family):
 # our arm
 
 
+def local_device() -> int:
+    """This rank's GPU (LOCAL_RANK; ranks share devices round-robin when
+    there are fewer GPUs than ranks, the gloo test mode)."""
+    import torch
+
+    return int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
+
+
 def run_step(torch, Engine, parse, wl, inputs, host=False, out_pinned=None, ctx=None):
     engine = Engine(parse(wl.program), schedule="stream", dist=ctx)
     for rel, t in inputs.items():
@@ -298,7 +306,7 @@ def bench_ours(args, rank, world, dist):
     from paper_2604_20073_b200 import Engine, parse
     from paper_2604_20073_b200 import device as dev
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(local_device())
     dev.lib()
     wl = make_workload(args.workload)
     inputs = wl.device_facts()
@@ -331,7 +339,7 @@ def bench_ours(args, rank, world, dist):
             jit_wait_s = time.perf_counter() - t0
     launches0 = dev.lib().srdl_launch_count()
     times = []
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0)), enabled=not os.environ.get("SRDL_BENCH_NO_CLOCKS")) as clocks:
+    with ClockSampler(local_device(), enabled=not os.environ.get("SRDL_BENCH_NO_CLOCKS")) as clocks:
         for _ in range(args.steps):
             gc.collect()  # release the previous step's engine before timing
             flush_l2(flush)
@@ -390,8 +398,9 @@ def bench_ours(args, rank, world, dist):
     e2e_s = sum(e2e_times) / len(e2e_times)
 
     tot_out = n_out  # relation sizes are global (the engine all-reduces them)
-    if dist:
-        t = torch.tensor([step_s, e2e_s], dtype=torch.float64, device="cuda")
+    if dist:  # max over ranks (host tensor for gloo)
+        t = torch.tensor([step_s, e2e_s], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         step_s, e2e_s = t.tolist()
     result = {
@@ -620,8 +629,10 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        # NCCL over NVLink on a multi-GPU box; SRDL_DIST_BACKEND=gloo runs the
+        # same multi-rank path with ranks sharing one GPU (tests of the bench)
+        tdist.init_process_group(os.environ.get("SRDL_DIST_BACKEND", "nccl"))
         dist = tdist
     result, wl, inputs, ctx = bench_ours(args, rank, world, dist)
     if not args.no_parity:

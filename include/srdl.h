@@ -88,6 +88,24 @@ int srdl_sort_dedup(const uint32_t *const *cols, uint32_t arity, uint64_t n, uin
 int srdl_sort_reorder(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits, uint32_t nkey,
                       uint32_t *const *out, void *stream);
 
+/* Compute Delta through a device hash set of the full relation (csrc/
+ * hashset.cu; reference storage.compute_delta, storage.py:311-324). `slots`
+ * is an open-addressing set of 2^log2cap packed row keys (UINT64_MAX =
+ * empty; keys are rows packed column 0 first with `bits` bits per column,
+ * arity * bits <= 63).
+ * srdl_hset_insert: add n rows.
+ * srdl_hset_filter: the packed keys of the staged rows NOT in the set,
+ *   compacted into keys_out (capacity n, any order), their count into
+ *   *count_dev (device) — only they need sorting.
+ * srdl_sort_unique_keys: sort m packed keys in place, drop duplicates and
+ *   unpack the distinct rows into out (capacity m); count into *count_dev. */
+int srdl_hset_insert(uint64_t *slots, uint32_t log2cap, const uint32_t *const *cols, uint32_t arity, uint64_t n,
+                     uint32_t bits, void *stream);
+int srdl_hset_filter(const uint32_t *const *cols, uint32_t arity, uint64_t n, uint32_t bits, const uint64_t *slots,
+                     uint32_t log2cap, uint64_t *keys_out, uint32_t *count_dev, void *stream);
+int srdl_sort_unique_keys(uint64_t *keys, uint64_t m, uint32_t arity, uint32_t bits, uint32_t *const *out,
+                          uint32_t *count_dev, void *stream);
+
 /* reference: storage.compute_delta (storage.py:311): distinct staged rows
  * minus the rows of up to eight sorted, duplicate-free segments (the full
  * relation's head and body, plus deltas of earlier chunks when a staging

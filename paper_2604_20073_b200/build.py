@@ -18,8 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsrdl.so")
-SOURCES = ["scan.cu", "sort.cu", "setops.cu", "wcoj.cu", "wcoj_mode0.cu", "wcoj_mode1.cu", "wcoj_mode2.cu",
-           "wcoj_jit.cu"]
+SOURCES = ["scan.cu", "sort.cu", "setops.cu", "hashset.cu", "wcoj.cu", "wcoj_mode0.cu", "wcoj_mode1.cu",
+           "wcoj_mode2.cu", "wcoj_jit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIBS = ["-ldl"]  # NVRTC is opened with dlopen (csrc/wcoj_jit.cu)
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]

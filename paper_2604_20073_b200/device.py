@@ -132,6 +132,12 @@ _SIGNATURES = {
     "srdl_sort_reorder": (
         C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p]
     ),
+    "srdl_hset_insert": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32,
+                                   C.c_void_p]),
+    "srdl_hset_filter": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_uint32,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
+    "srdl_sort_unique_keys": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]),
     "srdl_compute_delta": (
         C.c_int,
         [C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p, C.c_uint32,
@@ -491,6 +497,53 @@ def sort_reorder(rows: torch.Tensor, bits: int, order) -> torch.Tensor:
         col_ptrs(rows, order), arity, n, bits, nkey, col_ptrs(out), stream_handle()))
     check(rc, "sort_reorder")
     return out
+
+
+class HashSet:
+    """Device hash set of a relation's packed rows (csrc/hashset.cu): the
+    full relation's membership test for Compute Delta, kept up to date by
+    inserting each delta. Capacity a power of two, at most half full."""
+
+    def __init__(self, arity: int, bits: int, expect: int):
+        self.arity, self.bits = arity, bits
+        self.log2cap = max(10, int(2 * max(expect, 1) - 1).bit_length())
+        self.slots = torch.full((1 << self.log2cap,), -1, dtype=torch.int64, device=device())
+        self.size = 0
+
+    def fits(self, extra: int) -> bool:
+        return 2 * (self.size + extra) <= (1 << self.log2cap)
+
+    def insert(self, rows: torch.Tensor):
+        n = rows.shape[1]
+        if n:
+            _uses(rows, self.slots)
+            rc, _ = timed("compute_delta", 4 * self.arity * n + 8 * n, lambda: lib().srdl_hset_insert(
+                self.slots.data_ptr(), self.log2cap, col_ptrs(rows), self.arity, n, self.bits, stream_handle()))
+            check(rc, "hset_insert")
+            self.size += n
+
+    def filter(self, rows: torch.Tensor, count_slot: torch.Tensor):
+        """(u64 keys of the rows not in the set, compacted, capacity n; their
+        count lands in count_slot) — no host round trip."""
+        n = rows.shape[1]
+        keys = torch.empty(max(n, 1), dtype=torch.int64, device=device())
+        _uses(rows, self.slots, keys)
+        rc, _ = timed("compute_delta", 4 * self.arity * n + 8 * n, lambda: lib().srdl_hset_filter(
+            col_ptrs(rows) if n else None, self.arity, n, self.bits, self.slots.data_ptr(), self.log2cap,
+            keys.data_ptr(), count_slot.data_ptr(), stream_handle()))
+        check(rc, "hset_filter")
+        return keys
+
+
+def sort_unique_keys(keys: torch.Tensor, m: int, arity: int, bits: int, count_slot: torch.Tensor):
+    """Distinct rows (arity, capacity m) of m packed keys, sorted; the row
+    count lands in count_slot."""
+    out = empty_rows(arity, m)
+    _uses(keys, out)
+    rc, rec = timed("compute_delta", 16 * m, lambda: lib().srdl_sort_unique_keys(
+        keys.data_ptr(), m, arity, bits, col_ptrs(out) if m else None, count_slot.data_ptr(), stream_handle()))
+    check(rc, "sort_unique_keys")
+    return out, rec
 
 
 def compute_delta(rows: torch.Tensor, segments, bits: int = 32) -> torch.Tensor:

@@ -9,8 +9,10 @@ local = u - C[k-1], i1 = local // d2(k), i2 = local % d2(k).
 
 This module is the host (numpy) form of that arithmetic, kept so the
 reference's partition API (reference: pkg/src/flatlog/executor.py:45-150)
-is available unchanged; the device count/materialize kernels evaluate the
-same formulas per warp (csrc/wcoj.cu, `slice_of_warp` and `next_rect`).
+is available unchanged; the device kernels evaluate the same formulas per
+slice (csrc/wcoj_kernel.cuh: `wcoj_body` finds kappa by binary search on
+the prefix and cuts the slice into at most three rectangles per key;
+`run_rect` walks one rectangle).
 """
 
 from __future__ import annotations

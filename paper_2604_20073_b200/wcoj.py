@@ -10,7 +10,8 @@ step running in libsrdl:
 * histogram  root work space: outer histogram (maintained incrementally by
              the storage layer, or rebuilt over a constant-narrowed range),
              inner degrees d2 and the inclusive prefix of outer * d2;
-* count      csrc/wcoj.cu count kernel over p warp slices + exclusive scan;
+* count      the per-rule (csrc/wcoj_jit.cu) or generic (csrc/wcoj_kernel.cuh)
+             count kernel over the root slices + exclusive scan;
 * allocate   one exactly-sized output buffer (the only host sync);
 * materialize the same walk writing at the per-warp offsets.
 
@@ -297,7 +298,7 @@ class DevicePartition:
         )
 
     def slices_used(self) -> int:
-        """Slices the kernels cut [0, T) into (csrc/wcoj.cu `used`)."""
+        """Slices the kernels cut [0, T) into (csrc/wcoj_kernel.cuh `slices_used`)."""
         used = max(-(-self.total // MIN_SLICE_UNITS), min(self.nwarps * 4, self.total))
         return min(max(used, 1), self.nslices)
 

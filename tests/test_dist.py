@@ -162,3 +162,24 @@ def test_doop_200k_methods_ranks_match_single_gpu(world, tmp_path):
     iters = max(rounds)
     print(f"\nDOOP 200K methods, {world} ranks: max per-rank payload sent {sent / 1e6:.1f} MB over "
           f"{iters} iterations ({sent / iters / 1e6:.2f} MB/iteration, {exchanges} exchanges)")
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_gloo_one_gpu():
+    """bench.py's multi-rank path (torchrun, max-over-ranks timing, the
+    distributed engine, parity of the gathered output) with two ranks
+    sharing one GPU over gloo: TC (configs[0]) matches its committed digest."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRDL_DIST_BACKEND="gloo", SRDL_BENCH_NO_CLOCKS="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--workload",
+                          "tc", "--steps", "1", "--warmup", "3", "--profile-steps", "1", "--gpus", "2"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["parity"]["match"] is True
+    assert line["config"]["derived_tuples"] == 98_644_628

@@ -32,7 +32,7 @@ def run(source, facts, **kw):
 @pytest.mark.parametrize("schedule,general", [("seq", "0"), ("stream", "0"), ("stream", "1")])
 def test_golden_fixpoints(golden, schedule, general, monkeypatch):
     # general=1: every plan through the general kernel instance instead of
-    # the depth-specialised ones (csrc/wcoj.cu plan_kind)
+    # the depth-specialised ones (csrc/wcoj_launch.cuh plan_kind)
     monkeypatch.setenv("SRDL_WCOJ_GENERAL", general)
     records = golden("fixpoints.json.gz")
     for rec in records:
@@ -256,7 +256,7 @@ Tri(x, y, z) :- A(x, y), B(y, z), A(z, x).
 def test_sparse_ids_two_level_histogram_search():
     """Ids spread over 2^23 so no dense CSR offsets are built: every
     column-0 lookup goes through the index histogram's fence keys and one
-    64-key block (csrc/wcoj.cu hist_range); results vs the oracle."""
+    64-key block (csrc/wcoj_kernel.cuh hist_range); results vs the oracle."""
     from paper_2604_20073_b200 import Engine
 
     rng = np.random.default_rng(5)
@@ -367,3 +367,33 @@ def test_speculative_count_and_spills_match(monkeypatch, program, spec_bytes):
     got = engine.relation_columns(out).cpu().numpy().astype(np.int64).T
     assert len(want[out]) > 100
     assert np.array_equal(got, want[out])
+
+
+@pytest.mark.parametrize("program", ["tc", "sg", "andersen", "doop"])
+def test_hashed_compute_delta_vs_oracle(program, monkeypatch):
+    """Compute Delta through the device hash set of the full relation
+    (csrc/hashset.cu) on every iteration (thresholds lowered to 0), against
+    the oracle: the set is built, probed, grown and kept in step with every
+    merged delta."""
+    from oracle import native
+    from paper_2604_20073_b200 import Engine, suites
+    from paper_2604_20073_b200.fixpoint import Engine as E
+
+    monkeypatch.setattr(E, "HASH_MIN_FULL", 0)
+    monkeypatch.setattr(E, "HASH_MIN_STAGED", 0)
+    facts = {"tc": lambda: suites.tc_random(700, 3_500, seed=9),
+             "sg": lambda: suites.sg_layered(levels=16, width=500, seed=9),
+             "andersen": lambda: suites.andersen_modular(30_000, seed=9),
+             "doop": lambda: suites.doop_modular(12_000, seed=9)}[program]()
+    src, out = suites.BASELINE_PROGRAMS[program]
+    eng = Engine(parse(src), schedule="stream")
+    for rel, cols in facts.items():
+        eng.load_columns(rel, torch.from_numpy(cols).cuda())
+    summary = eng.solve()
+    top = max(int(v.max()) for v in facts.values()) + 1
+    want, rep = native.fixpoint(parse(src), {k: v.T for k, v in facts.items()}, Symbols(top))
+    for rel in parse(src).declarations:
+        got = eng.relation_columns(rel).cpu().numpy().astype(np.int64).T
+        assert np.array_equal(got, want[rel]), (program, rel)
+    if not parse(src).splits:
+        assert sorted(summary.rounds_by_rules().values()) == sorted(r for _, _, r in rep)
