@@ -42,9 +42,16 @@ def main():
     step()
     dev.jit_wait()
     step()
+    keys = ("num_alloc_retries", "num_sync_all_streams", "num_device_alloc", "num_device_free",
+            "allocation.all.allocated")
+    m0 = torch.cuda.memory_stats()
     t0 = time.perf_counter()
     step()
     plain = time.perf_counter() - t0
+    m1 = torch.cuda.memory_stats()
+    print("allocator over one fixpoint:", {k: m1.get(k, 0) - m0.get(k, 0) for k in keys},
+          "reserved GB", round(m1.get("reserved_bytes.all.current", 0) / 1e9, 1),
+          "alloc conf", os.environ.get("PYTORCH_CUDA_ALLOC_CONF"))
     prof = cProfile.Profile()
     prof.enable()
     step()
