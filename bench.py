@@ -225,6 +225,36 @@ def profile_traffic(workload_name, family):
     return (d.get(workload_name) or {}).get(family)
 
 
+def profile_issue(workload_name, family, live_launch_ms, launches_per_step):
+    """Issue-rate roofline of a latency-bound family (the WCOJ walk moves a
+    few hundred GB/s of algorithmic bytes: HBM is not what bounds it): warp
+    instructions per launch from the committed `ncu --set full` capture
+    (profiles/r02/issue.json, tools/ncu_summary.py --json) against the SM
+    issue peak, 148 SMs x 4 schedulers x 1 warp instruction per cycle at the
+    maximum SM clock. When the step has one launch of the family, the live
+    launch time gives the achieved rate; otherwise the capture's own."""
+    path = os.path.join(ROOT, "profiles", "r02", "issue.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        d = (json.load(fh).get(workload_name) or {}).get(family)
+    if not d:
+        return None
+    mhz = 1965.0
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as fh:
+            mhz = float(json.load(fh).get("sm_max_mhz", mhz))
+    peak = 148 * 4 * mhz * 1e6 / 1e9  # G warp instructions / s
+    live = launches_per_step == 1 and live_launch_ms
+    ms = live_launch_ms if live else d["duration_ms"]
+    achieved = d["inst_executed"] / (ms * 1e-3) / 1e9
+    return {"bound": "issue", "unit": "G warp-inst/s", "achieved": round(achieved, 1), "peak": round(peak, 1),
+            "frac": round(achieved / peak, 4), "inst_per_launch": d["inst_executed"],
+            "time_source": "live launch time (CUDA events)" if live else "ncu duration of the captured launches",
+            "ncu_issue_active_pct": d.get("issue_active_pct"), "source": d.get("source")}
+
+
 # --------------------------------------------------------------------------
 # our arm
 
@@ -271,6 +301,7 @@ def family_roofline(records, steps, step_s, wl_name):
     t, n, by = fam[name]
     peak, src = measured_peaks()
     achieved = by / t / 1e9 if t > 0 else 0.0
+    issue = profile_issue(wl_name, name, t / n * 1e3, n / steps)
     return {
         "bound": "hbm",
         "kernel": name,
@@ -295,6 +326,7 @@ def family_roofline(records, steps, step_s, wl_name):
         "families_ms_per_step": {k: round(v[0] / steps * 1e3, 3) for k, v in
                                  sorted(fam.items(), key=lambda kv: -kv[1][0])},
         "families_gbs": {k: round(v[2] / v[0] / 1e9, 1) for k, v in fam.items() if v[0] > 0},
+        "issue_roofline": issue,
         "note": "family = one libsrdl C-ABI call (one or more kernels); times are CUDA events on the "
                 "launching stream, so families on concurrent streams overlap and shares can sum past 1",
     }

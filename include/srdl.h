@@ -62,6 +62,12 @@ const char *srdl_last_error(void);
 int srdl_sm_count(void);
 /* Kernels launched by this library since load (process-wide counter). */
 uint64_t srdl_launch_count(void);
+/* Work launched on `waiter` after this call starts after all work launched on
+ * `signaler` before it (event record + stream wait; the engine's fork/join of
+ * side streams — reference runtime.py:225-257 runs phases of independent
+ * plans concurrently; this is the device-side ordering that replaces its
+ * thread-pool join). */
+int srdl_stream_wait(void *waiter, void *signaler);
 /* Device-wide prefix sums (exclusive or inclusive; total = sum, exclusive
  * only, device pointer or NULL). in and out may alias. */
 int srdl_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, int exclusive, uint32_t *total, void *stream);

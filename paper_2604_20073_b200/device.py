@@ -123,6 +123,7 @@ _SIGNATURES = {
     "srdl_last_error": (C.c_char_p, []),
     "srdl_sm_count": (C.c_int, []),
     "srdl_launch_count": (C.c_uint64, []),
+    "srdl_stream_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
     "srdl_scan_u32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
     "srdl_scan_u64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]),
     "srdl_sort_dedup": (
@@ -334,6 +335,12 @@ def _uses(*tensors):
         for t in tensors:
             if t is not None and t.numel():
                 t.record_stream(s)
+
+
+def stream_wait(waiter, signaler):
+    """Order `waiter` after the work launched so far on `signaler` (torch
+    Streams; libsrdl's event ring instead of Stream.wait_stream)."""
+    check(_LIB.srdl_stream_wait(waiter.cuda_stream, signaler.cuda_stream), "stream_wait")
 
 
 def stream_handle() -> int:

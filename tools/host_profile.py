@@ -41,7 +41,8 @@ def main():
 
     step()
     dev.jit_wait()
-    step()
+    for _ in range(4):  # steady state: the allocator's cache and the pools have grown
+        step()
     keys = ("num_alloc_retries", "num_sync_all_streams", "num_device_alloc", "num_device_free",
             "allocation.all.allocated")
     m0 = torch.cuda.memory_stats()

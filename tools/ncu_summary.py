@@ -1,7 +1,10 @@
 """Key counters of an `ncu --set full` report, one block per profiled launch:
-    python tools/ncu_summary.py REPORT.ncu-rep"""
+    python tools/ncu_summary.py REPORT.ncu-rep [--json OUT.json]
+--json also writes, per launch, the figures bench.py's issue-rate roofline
+reads (profiles/r02/issue.json): duration, warp instructions, issue-active."""
 import csv
 import io
+import json
 import subprocess
 import sys
 
@@ -28,9 +31,25 @@ def main():
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
+    launches = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         u = dict(zip(hdr, units))
+
+        def num(k):
+            try:
+                return float(d[k].replace(",", ""))
+            except (KeyError, ValueError):
+                return None
+
+        dur = num("gpu__time_duration.sum")
+        scale = {"ms": 1.0, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "nsecond": 1e-6}.get(
+            u.get("gpu__time_duration.sum", "ms"), 1.0)
+        launches.append({"kernel": d.get("Kernel Name", "?")[:90],
+                         "duration_ms": dur * scale if dur is not None else None,
+                         "inst_executed": num("smsp__inst_executed.sum"),
+                         "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                         "sm_cycles_active_avg": num("sm__cycles_active.avg")})
         print(f"== {d.get('Kernel Name', '?')[:90]}")
         for k in WANT:
             if k in d:
@@ -51,6 +70,9 @@ def main():
         tot = sum(s for s, _ in stalls) or 1.0
         if stalls:
             print("  warp-stall samples: " + ", ".join(f"{n} {100 * s / tot:.1f}%" for s, n in sorted(stalls, reverse=True)[:8]))
+    if "--json" in sys.argv:
+        with open(sys.argv[sys.argv.index("--json") + 1], "w") as fh:
+            json.dump(launches, fh, indent=1)
 
 
 if __name__ == "__main__":
