@@ -9,6 +9,7 @@ import os
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")  # as bench.py
 
 import argparse  # noqa: E402
+import gc
 import cProfile
 import io
 import pstats
@@ -33,6 +34,7 @@ def main():
     facts = wl.device_facts()
 
     def step():
+        gc.collect()  # as bench.py: the previous engine's memory back to the allocator first
         eng = Engine(parse(wl.program), schedule="stream")
         for k, v in facts.items():
             eng.load_columns(k, v)
