@@ -169,8 +169,17 @@ namespace srdl {
 // total_dev (device pointer, may be null). in and out may alias.
 void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *total_dev,
                         cudaStream_t s);
+// the same over the first min(n, *bound) values, bound a device word (the
+// count is produced by an earlier kernel of the stream; no host round trip)
+void exclusive_scan_u64_bounded(const uint64_t *in, uint64_t *out, uint64_t n, const uint64_t *bound,
+                                uint64_t *total_dev, cudaStream_t s);
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *total_dev,
                         cudaStream_t s);
+// the onesweep passes' (tile, digit) look-back words, persistent per
+// (device, stream, thread) and never cleared: every pass gets a fresh epoch
+// (1 .. kOnesweepEpochs - 1) that its words carry in bits 32-61
+constexpr uint32_t kOnesweepEpochs = 1u << 30;
+uint64_t *onesweep_status(cudaStream_t s, size_t words, uint32_t *epoch);
 void inclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, cudaStream_t s);
 // stable radix sort of keys (and optional 32-bit values) on key bits
 // [lo_bit, lo_bit + bits); results land back in keys/vals.

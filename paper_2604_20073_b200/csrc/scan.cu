@@ -255,12 +255,25 @@ __device__ __forceinline__ T wsum_total(const T *wsum) {
 template <class T, bool EXCLUSIVE>
 __global__ void __launch_bounds__(kThreads)
     chained_scan(const T *__restrict__ in, T *__restrict__ out, uint64_t n, T *__restrict__ total,
-                 uint64_t *status, uint64_t *value, uint64_t cap, uint64_t epoch) {
+                 uint64_t *status, uint64_t *value, uint64_t cap, uint64_t epoch,
+                 const uint64_t *__restrict__ bound) {
     __shared__ T wsum[kWarps];
     __shared__ T wbase[kWarps];
     __shared__ uint64_t tile_excl;
     const uint64_t tile = blockIdx.x;  // blocks are dispatched in index order
     const uint64_t base = tile * kTile;
+    // bound (device word, optional): scan only [0, min(n, *bound)); tiles
+    // past it return before publishing (no later tile looks back on them)
+    if (bound) {
+        const uint64_t b = *bound;
+        if (b < n) n = b;
+        if (n == 0) {
+            if (total && tile == 0 && threadIdx.x == 0) *total = 0;
+            return;
+        }
+        if (base >= n) return;
+    }
+    const uint64_t last_tile = (n - 1) / kTile;
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
     T x[kItems];
 #pragma unroll
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(kThreads)
         const uint64_t i = base + (uint64_t)w * kWarpChunk + r * 32 + l;
         if (i < n) out[i] = v[r] + add;
     }
-    if (total && tile == gridDim.x - 1 && threadIdx.x == 0) *total = (T)(tile_excl + wsum_total(wsum));
+    if (total && tile == last_tile && threadIdx.x == 0) *total = (T)(tile_excl + wsum_total(wsum));
 }
 
 namespace {
@@ -373,10 +386,49 @@ ScanState &scan_state(cudaStream_t s, size_t tiles) {
     return st;
 }
 
+// persistent per-(tile, digit) look-back status of the onesweep radix passes
+// (sort.cu), per (device, stream, thread); epoch-stamped like the scan's
+struct SortStatus {
+    uint64_t *words = nullptr;
+    size_t cap = 0;
+    uint32_t epoch = 0;
+};
+std::unordered_map<ArenaKey, SortStatus, ArenaKeyHash> g_sort_status;
+
 }  // namespace
 
+uint64_t *onesweep_status(cudaStream_t s, size_t words, uint32_t *epoch) {
+    const ArenaKey key = arena_key(s);
+    std::lock_guard<std::mutex> lock(g_scan_mu);
+    SortStatus &st = g_sort_status[key];
+    if (st.cap < words) {
+        // old buffers may still be read by queued passes of this stream: leaked
+        size_t cap = st.cap ? st.cap : (size_t)1 << 16;
+        while (cap < words) cap *= 2;
+        SRDL_CUDA(cudaMalloc(&st.words, cap * sizeof(uint64_t)));
+        SRDL_CUDA(cudaMemsetAsync(st.words, 0, cap * sizeof(uint64_t), s));  // epoch 0: never published
+        st.cap = cap;
+        st.epoch = 0;
+    }
+    if (++st.epoch >= kOnesweepEpochs) {  // the 30-bit epoch wrapped: start over from a clear buffer
+        SRDL_CUDA(cudaMemsetAsync(st.words, 0, st.cap * sizeof(uint64_t), s));
+        st.epoch = 1;
+    }
+    *epoch = st.epoch;
+    return st.words;
+}
+
 template <class T, bool EXCLUSIVE>
-static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s) {
+static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s, const uint64_t *bound = nullptr) {
+    if (n && bound) {  // the element count is only known on the device: the chained kernel always
+        const uint64_t blocks = (n + kTile - 1) / kTile;
+        ScanState &st = scan_state(s, blocks);
+        const uint64_t epoch = ++st.epoch;
+        chained_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, total, st.status, st.value,
+                                                                           st.cap, epoch, bound);
+        SRDL_CHECK_LAUNCH();
+        return;
+    }
     if (n == 0) {
         if (total) {
             write_zero<T><<<1, 1, 0, s>>>(total);
@@ -393,13 +445,17 @@ static void scan_impl(const T *in, T *out, uint64_t n, T *total, cudaStream_t s)
     ScanState &st = scan_state(s, blocks);
     const uint64_t epoch = ++st.epoch;
     chained_scan<T, EXCLUSIVE><<<(unsigned)blocks, kThreads, 0, s>>>(in, out, n, total, st.status, st.value, st.cap,
-                                                                       epoch);
+                                                                       epoch, nullptr);
     SRDL_CHECK_LAUNCH();
 }
 
 void exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *total,
                         cudaStream_t s) {
     scan_impl<uint64_t, true>(in, out, n, total, s);
+}
+void exclusive_scan_u64_bounded(const uint64_t *in, uint64_t *out, uint64_t n, const uint64_t *bound,
+                                uint64_t *total, cudaStream_t s) {
+    scan_impl<uint64_t, true>(in, out, n, total, s, bound);
 }
 void exclusive_scan_u32(const uint32_t *in, uint32_t *out, uint64_t n, uint32_t *total,
                         cudaStream_t s) {

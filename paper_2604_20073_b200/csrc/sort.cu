@@ -18,10 +18,11 @@ constexpr int kBins = 1 << kRadixBits;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWarpChunk = 32 * kItems;
 constexpr int kMaxPasses = 8;  // 64-bit keys
+#ifndef SRDL_SORT_ITEMS_DEFAULT
+#define SRDL_SORT_ITEMS_DEFAULT 16
+#endif
+constexpr int kDefaultSortItems = SRDL_SORT_ITEMS_DEFAULT;
 
-__device__ __forceinline__ uint64_t tile_index(uint64_t tile, int w, int r, int l) {
-    return tile * kTile + (uint64_t)w * kWarpChunk + r * 32 + l;
-}
 
 // Onesweep LSD radix sort (decoupled look-back, Merrill & Garland's single-
 // pass prefix scan applied per digit): one histogram pass over the keys
@@ -80,10 +81,15 @@ __global__ void radix_digit_starts(uint32_t *hist, int passes, const int *__rest
     }
 }
 
-// look-back status word per (tile, digit): flag in the top two bits
+// look-back status word per (tile, digit): flag in the top two bits, the
+// pass's epoch in bits 32-61, the count in bits 0-31 (n < 2^32). The words
+// persist across passes and sorts (onesweep_status): a word of an earlier
+// pass carries another epoch and reads as "not published", so no pass
+// clears them first.
 constexpr uint64_t kFlagAgg = 1ull << 62;  // this tile's own count is published
 constexpr uint64_t kFlagInc = 2ull << 62;  // inclusive prefix through this tile
-constexpr uint64_t kValMask = (1ull << 62) - 1;
+constexpr uint64_t kValMask = 0xffffffffull;
+constexpr uint64_t kEpochMask = (1ull << 30) - 1;
 
 // Lanes of the warp holding the same digit as this lane (invalid lanes,
 // digit kBins, group among themselves): one ballot per digit bit instead of
@@ -99,23 +105,34 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool ok) {
     return peers;
 }
 
-template <bool HAS_VALS>
-constexpr size_t onesweep_smem() {
-    return (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0) + (size_t)kWarps * kBins * 4 +
-           (size_t)kBins * 8 + 64 * 4 + 16;
+// ITEMS keys per thread, a tile of kThreads * ITEMS keys. 16 items: 128
+// registers, 2 blocks (25 % of the warp slots) per SM; 8 items: 4 blocks.
+// ncu (TC, 113 M keys per pass, 16 items): issue-bound at 25 % occupancy
+// (issue active 48 %, DRAM 20 % of peak, 169 instructions per key).
+template <int ITEMS>
+constexpr int onesweep_min_blocks() {
+    return ITEMS >= 16 ? 2 : 4;
 }
 
-template <bool HAS_VALS>
-__global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per thread
+template <bool HAS_VALS, int ITEMS>
+constexpr size_t onesweep_smem() {
+    return (size_t)kThreads * ITEMS * 8 + (HAS_VALS ? (size_t)kThreads * ITEMS * 4 : 0) +
+           (size_t)kWarps * kBins * 4 + (size_t)kBins * 8 + 64 * 4 + 16;
+}
+
+template <bool HAS_VALS, int ITEMS>
+__global__ void __launch_bounds__(kThreads, onesweep_min_blocks<ITEMS>())
     onesweep_pass(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n, int shift,
-                  const uint32_t *__restrict__ starts, uint64_t *status, uint32_t *tile_ticket,
+                  const uint32_t *__restrict__ starts, uint64_t *status, uint64_t epoch, uint32_t *tile_ticket,
                   uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
                   const int *__restrict__ unsorted) {
     if (unsorted && *unsorted == 0) return;
+    constexpr int kI = ITEMS;
+    constexpr uint32_t kT = (uint32_t)kThreads * ITEMS;  // keys per tile
     extern __shared__ __align__(16) unsigned char sm[];
     uint64_t *skeys = (uint64_t *)sm;
-    uint32_t *svals = (uint32_t *)(sm + (size_t)kTile * 8);
-    uint32_t(*cnt)[kBins] = (uint32_t(*)[kBins])(sm + (size_t)kTile * 8 + (HAS_VALS ? (size_t)kTile * 4 : 0));
+    uint32_t *svals = (uint32_t *)(sm + (size_t)kT * 8);
+    uint32_t(*cnt)[kBins] = (uint32_t(*)[kBins])(sm + (size_t)kT * 8 + (HAS_VALS ? (size_t)kT * 4 : 0));
     int64_t *gbase = (int64_t *)((unsigned char *)cnt + (size_t)kWarps * kBins * 4);
     uint32_t *wsum = (uint32_t *)(gbase + kBins);  // [kWarps] scan carries
     uint32_t *tile_slot = wsum + 64;
@@ -126,22 +143,22 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
     for (int i = threadIdx.x; i < kWarps * kBins; i += kThreads) (&cnt[0][0])[i] = 0;
     __syncthreads();
     const uint64_t tile = *tile_slot;
-    uint64_t k[kItems];
-    uint32_t v[kItems];
-    uint32_t rank[kItems];
+    uint64_t k[kI];
+    uint32_t v[kI];
+    uint32_t rank[kI];
     const uint32_t lt = (1u << l) - 1u;
     // all of the thread's keys in flight at once (the ranking loop below
     // serialises on shared memory; loading inside it left one global load
     // outstanding per warp: 45 % of stall samples on the key's first use)
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const uint64_t i = tile_index(tile, w, r, l);
+    for (int r = 0; r < kI; ++r) {
+        const uint64_t i = (tile * kT + (uint64_t)w * (32 * kI) + r * 32 + l);
         k[r] = i < n ? __ldcs(keys + i) : 0;
         if (HAS_VALS) v[r] = i < n ? __ldcs(vals + i) : 0;
     }
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const uint64_t i = tile_index(tile, w, r, l);
+    for (int r = 0; r < kI; ++r) {
+        const uint64_t i = (tile * kT + (uint64_t)w * (32 * kI) + r * 32 + l);
         const bool ok = i < n;
         const uint32_t d = ok ? (uint32_t)((k[r] >> shift) & (kBins - 1)) : (uint32_t)kBins;
         const uint32_t peers = digit_peers(d, ok);
@@ -166,10 +183,11 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
     }
     // publish this tile's count, then look back for the digit's prefix
     uint64_t *st = status + tile * kBins + d;
+    const uint64_t stamp = epoch << 32;
     if (tile == 0) {
-        *(volatile uint64_t *)st = kFlagInc | total;
+        *(volatile uint64_t *)st = kFlagInc | stamp | total;
     } else {
-        *(volatile uint64_t *)st = kFlagAgg | total;
+        *(volatile uint64_t *)st = kFlagAgg | stamp | total;
     }
     uint64_t excl = 0;
     if (tile > 0) {
@@ -184,13 +202,15 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
             uint64_t sw[kLook];
 #pragma unroll
             for (int j = 0; j < kLook; ++j)
-                sw[j] = t - j >= 0 ? *(volatile uint64_t *)(status + (uint64_t)(t - j) * kBins + d) : (2ull << 62);  // before tile 0: an empty inclusive prefix
+                sw[j] = t - j >= 0 ? *(volatile uint64_t *)(status + (uint64_t)(t - j) * kBins + d)
+                                   : (kFlagInc | stamp);  // before tile 0: an empty inclusive prefix
             int j = 0;
             bool done = false;
 #pragma unroll
             for (int q = 0; q < kLook; ++q) {
                 if (done || j != q) continue;
-                if ((sw[q] & ~kValMask) == 0) continue;  // not published yet: retry from here
+                // not published in this pass yet (an older epoch): retry from here
+                if (((sw[q] >> 32) & kEpochMask) != epoch || (sw[q] >> 62) == 0) continue;
                 excl += sw[q] & kValMask;
                 ++j;
                 done = (sw[q] & kFlagInc) != 0;
@@ -198,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
             if (done) break;
             t -= j;
         }
-        *(volatile uint64_t *)st = kFlagInc | (excl + total);
+        *(volatile uint64_t *)st = kFlagInc | stamp | (excl + total);
     }
     uint32_t incl = total;  // block-wide inclusive scan of the digit totals
 #pragma unroll
@@ -216,8 +236,8 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
     gbase[d] = (int64_t)starts[d] + (int64_t)excl - (int64_t)local_start;
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const uint64_t i = tile_index(tile, w, r, l);
+    for (int r = 0; r < kI; ++r) {
+        const uint64_t i = (tile * kT + (uint64_t)w * (32 * kI) + r * 32 + l);
         if (i < n) {
             const uint32_t dd = (uint32_t)((k[r] >> shift) & (kBins - 1));
             const uint32_t lpos = cnt[w][dd] + rank[r];
@@ -226,8 +246,8 @@ __global__ void __launch_bounds__(kThreads, 2)  // 16 keys (+ values) live per t
         }
     }
     __syncthreads();
-    const uint64_t base = tile * kTile;
-    const uint32_t here = n - base < (uint64_t)kTile ? (uint32_t)(n - base) : (uint32_t)kTile;
+    const uint64_t base = tile * kT;
+    const uint32_t here = n - base < (uint64_t)kT ? (uint32_t)(n - base) : (uint32_t)kT;
     for (uint32_t i = threadIdx.x; i < here; i += kThreads) {
         const uint64_t key = skeys[i];
         const uint32_t dd = (uint32_t)((key >> shift) & (kBins - 1));
@@ -246,6 +266,16 @@ __global__ void copy_if_unsorted(T *__restrict__ dst, const T *__restrict__ src,
         dst[i] = src[i];
 }
 
+// keys per thread of the onesweep passes: SRDL_SORT_ITEMS=8|16 (A/B knob)
+static int sort_items() {
+    static int items = [] {
+        const char *v = getenv("SRDL_SORT_ITEMS");
+        const int x = v && *v ? atoi(v) : kDefaultSortItems;
+        return x == 8 ? 8 : 16;
+    }();
+    return items;
+}
+
 // `unsorted` (optional device flag): when it reads 0 every pass returns at
 // once and the keys stay in place, so a caller can skip sorting already
 // ordered input without a host round trip.
@@ -254,26 +284,29 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
     if (n <= 1 || bits == 0) return;
     SRDL_REQUIRE(n < (1ull << 32), "radix_sort: %llu rows exceeds the 32-bit rank space",
                  (unsigned long long)n);
-    const uint64_t tiles = (n + kTile - 1) / kTile;
     const int passes = (int)((bits + kRadixBits - 1) / kRadixBits);
     SRDL_REQUIRE(passes <= kMaxPasses, "radix_sort: %u bits", bits);
     static uint64_t raised = 0;
     if (first_use_on_device(&raised)) {  // the reorder tile needs more than the 48 KB default
-        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)onesweep_smem<true>()));
-        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)onesweep_smem<false>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<true, 16>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<false, 16>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<true, 8>()));
+        SRDL_CUDA(cudaFuncSetAttribute(onesweep_pass<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)onesweep_smem<false, 8>()));
     }
+    const int items = sort_items();
+    const uint64_t tiles = (n + (uint64_t)kThreads * items - 1) / ((uint64_t)kThreads * items);
     Scratch kalt(n * sizeof(uint64_t), s);
     Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);
-    // digit counts of every pass and one tile ticket per pass (zeroed once),
-    // the look-back status of every (tile, digit) of the running pass
-    // (zeroed before each pass, stream-ordered after the previous one)
+    // digit counts of every pass and one tile ticket per pass (zeroed once);
+    // the look-back status of every (tile, digit) is the stream's persistent
+    // epoch-stamped buffer (never cleared; a fresh epoch per pass)
     const size_t hist_bytes = (size_t)kMaxPasses * kBins * sizeof(uint32_t);
     const size_t ticket_bytes = (size_t)kMaxPasses * sizeof(uint32_t);
-    const size_t status_bytes = (size_t)tiles * kBins * sizeof(uint64_t);
     Scratch meta(hist_bytes + ticket_bytes, s);
-    Scratch status(status_bytes, s);
     uint32_t *hist = meta.as<uint32_t>();
     uint32_t *tickets = hist + kMaxPasses * kBins;
     SRDL_CUDA(cudaMemsetAsync(hist, 0, hist_bytes + ticket_bytes, s));
@@ -286,14 +319,23 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
     uint32_t *vin = vals, *vout = vals ? valt.as<uint32_t>() : nullptr;
     for (int p = 0; p < passes; ++p) {
         const int shift = (int)lo_bit + p * kRadixBits;
-        SRDL_CUDA(cudaMemsetAsync(status.as<uint64_t>(), 0, status_bytes, s));
-        if (vals)
-            onesweep_pass<true><<<(unsigned)tiles, kThreads, onesweep_smem<true>(), s>>>(
-                kin, vin, n, shift, hist + p * kBins, status.as<uint64_t>(), tickets + p, kout, vout, unsorted);
-        else
-            onesweep_pass<false><<<(unsigned)tiles, kThreads, onesweep_smem<false>(), s>>>(
-                kin, nullptr, n, shift, hist + p * kBins, status.as<uint64_t>(), tickets + p, kout, nullptr,
-                unsorted);
+        uint32_t epoch = 0;
+        uint64_t *status = onesweep_status(s, (size_t)tiles * kBins, &epoch);
+        if (items == 8) {
+            if (vals)
+                onesweep_pass<true, 8><<<(unsigned)tiles, kThreads, onesweep_smem<true, 8>(), s>>>(
+                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted);
+            else
+                onesweep_pass<false, 8><<<(unsigned)tiles, kThreads, onesweep_smem<false, 8>(), s>>>(
+                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted);
+        } else {
+            if (vals)
+                onesweep_pass<true, 16><<<(unsigned)tiles, kThreads, onesweep_smem<true, 16>(), s>>>(
+                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted);
+            else
+                onesweep_pass<false, 16><<<(unsigned)tiles, kThreads, onesweep_smem<false, 16>(), s>>>(
+                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted);
+        }
         SRDL_CHECK_LAUNCH();
         std::swap(kin, kout);
         std::swap(vin, vout);

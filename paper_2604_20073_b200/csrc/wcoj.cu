@@ -60,6 +60,38 @@ __global__ void __launch_bounds__(256) gather_kernel(const srdl_exec X, const sr
     }
 }
 
+// Count prologue (one launch instead of four or five memsets over the whole
+// slice capacity): zero the slice ticket and the arena cursor / spill count,
+// compute the number of slices this launch uses (slices_used of the root
+// work total) into *used, and zero only those slices' counts and spill
+// flags — every reader (scan, gather, materialize) stops at the same bound.
+__global__ void __launch_bounds__(256) count_prologue(const srdl_exec X, const srdl_spec Q, int spec,
+                                                      uint64_t *used_out) {
+    const uint64_t T = X.nkeys ? X.prefix[X.nkeys - 1] : 0;
+    const uint64_t used = slices_used(X, T);
+    const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i0 == 0) {
+        *X.ticket = 0;
+        *used_out = used;
+        if (spec) {
+            *Q.cursor = 0;
+            *Q.spills = 0;
+        }
+    }
+    for (uint64_t i = i0; i < used; i += (uint64_t)gridDim.x * blockDim.x) {
+        X.slice_counts[i] = 0;
+        if (spec) Q.slice_spill[i] = 0;
+    }
+}
+
+static void count_prologue_launch(const srdl_exec *X, const srdl_spec *Q, uint64_t *used, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((X->nslices + 255) / 256 < (uint64_t)sm_count() * 4
+                                           ? (X->nslices + 255) / 256 : (uint64_t)sm_count() * 4);
+    srdl_spec none{};
+    count_prologue<<<blocks, 256, 0, s>>>(*X, Q ? *Q : none, Q != nullptr, used);
+    SRDL_CHECK_LAUNCH();
+}
+
 static void check_spec(const srdl_plan *P, const srdl_spec *Q) {
     SRDL_REQUIRE(Q != nullptr, "a speculative arena is required");
     SRDL_REQUIRE(Q->chunk >= 32 && (Q->chunk & (Q->chunk - 1)) == 0, "chunk %u: power of two >= 32", Q->chunk);
@@ -90,11 +122,12 @@ int srdl_wcoj_count(const srdl_plan *plan, const srdl_exec *ex, void *stream) {
     return guarded([&] {
         check_plan(plan, ex);
         cudaStream_t s = (cudaStream_t)stream;
-        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
-        SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
+        Scratch used(sizeof(uint64_t), s);
+        count_prologue_launch(ex, nullptr, used.as<uint64_t>(), s);
         launch<kCount>(plan, ex, nullptr, s);
         SRDL_CHECK_LAUNCH();
-        exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
+        exclusive_scan_u64_bounded(ex->slice_counts, ex->slice_offsets, ex->nslices, used.as<uint64_t>(),
+                                   ex->total, s);
     });
 }
 
@@ -103,15 +136,12 @@ int srdl_wcoj_count_spec(const srdl_plan *plan, const srdl_exec *ex, const srdl_
         check_plan(plan, ex);
         check_spec(plan, spec);
         cudaStream_t s = (cudaStream_t)stream;
-        SRDL_CUDA(cudaMemsetAsync(ex->ticket, 0, sizeof(uint32_t), s));
-        SRDL_CUDA(cudaMemsetAsync(ex->slice_counts, 0, ex->nslices * sizeof(uint64_t), s));
-        SRDL_CUDA(cudaMemsetAsync(spec->cursor, 0, sizeof(uint32_t), s));
-        SRDL_CUDA(cudaMemsetAsync(spec->spills, 0, sizeof(uint64_t), s));
-        // slices the launch never reaches (beyond the used count) are empty
-        SRDL_CUDA(cudaMemsetAsync(spec->slice_spill, 0, ex->nslices * sizeof(uint32_t), s));
+        Scratch used(sizeof(uint64_t), s);
+        count_prologue_launch(ex, spec, used.as<uint64_t>(), s);
         launch<kSpec>(plan, ex, spec, s);
         SRDL_CHECK_LAUNCH();
-        exclusive_scan_u64(ex->slice_counts, ex->slice_offsets, ex->nslices, ex->total, s);
+        exclusive_scan_u64_bounded(ex->slice_counts, ex->slice_offsets, ex->nslices, used.as<uint64_t>(),
+                                   ex->total, s);
     });
 }
 

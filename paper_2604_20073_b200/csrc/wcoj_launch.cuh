@@ -5,6 +5,9 @@
 
 #include <stdlib.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "wcoj_jit.h"
 #include "wcoj_kernel.cuh"
 
@@ -40,11 +43,37 @@ static size_t block_bytes(const srdl_plan *P) {
 // (X->nwarps, nslices, min_units) comes from the caller and is identical
 // for the count and the materialize launch; the grid is only how many warps
 // fetch those slices, so it never feeds into the slicing.
+// (memoised per kernel, shared-memory size and device: the occupancy query
+// is a driver call on every one of ~1,000 launches per DOOP fixpoint)
 static unsigned wave_blocks(const void *fn, size_t bytes) {
+    struct Key {
+        const void *fn;
+        size_t bytes;
+        int dev;
+        bool operator==(const Key &o) const { return fn == o.fn && bytes == o.bytes && dev == o.dev; }
+    };
+    struct KeyHash {
+        size_t operator()(const Key &k) const {
+            return std::hash<const void *>()(k.fn) ^ (k.bytes * 0x9e3779b97f4a7c15ull) ^ (size_t)k.dev;
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, unsigned, KeyHash> memo;
+    int dev = 0;
+    SRDL_CUDA(cudaGetDevice(&dev));
+    const Key key{fn, bytes, dev};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = memo.find(key);
+        if (it != memo.end()) return it->second;
+    }
     int per_sm = 0;
     SRDL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJoinWarps * 32, bytes));
     if (per_sm < 1) per_sm = 1;
-    return (unsigned)(per_sm * sm_count());
+    const unsigned blocks = (unsigned)(per_sm * sm_count());
+    std::lock_guard<std::mutex> lock(mu);
+    memo[key] = blocks;
+    return blocks;
 }
 
 template <int MODE, int KIND>
