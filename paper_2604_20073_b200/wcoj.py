@@ -568,6 +568,26 @@ class PlanExecution:
             self.prep.descriptor()
         return self.partition
 
+    # The stream schedule splits histogram() in two: sources + descriptor on
+    # the main stream, the root work space on the plan's side stream.
+
+    def prepare_sources(self):
+        self.prep = prepare(self.plan, self.store, self.interner, self.derived)
+        if self.plan.depth and self.prep.ok:
+            self.prep.descriptor()  # may build dense offsets other plans read: main stream
+        return self.prep
+
+    def needs_main_stream_partition(self) -> bool:
+        """The root work space launches nothing (no work) or needs torch ops
+        (a constant-led outer atom: its histogram is rebuilt over the
+        narrowed range), so it is built on the main stream."""
+        plan = self.plan
+        return plan.depth == 0 or not self.prep.ok or plan.atoms[plan.outer_atom].n_const > 0
+
+    def build_root_space(self):
+        self.partition = build_partition(self.plan, self.store, self.p, self.prep, dist=self.dist)
+        return self.partition
+
     def has_work(self) -> bool:
         """False when the count pass would launch nothing useful (an empty
         source or no root keys): the stream schedule then skips the plan

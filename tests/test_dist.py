@@ -23,7 +23,21 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _free_gpu():
+    """The ranks share this process's GPU: hand back the engine arenas, pools
+    and torch's cached blocks that earlier tests in this process hold."""
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        import gc
+
+        from paper_2604_20073_b200 import fixpoint
+
+        gc.collect()
+        fixpoint.release_arenas()
+        torch.cuda.empty_cache()
+
+
 def _spawn(fn, world, *args):
+    _free_gpu()
     port = _free_port()
     mp.spawn(fn, args=(world, port, *args), nprocs=world, join=True)
 
@@ -174,6 +188,7 @@ def test_bench_two_ranks_gloo_one_gpu():
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    _free_gpu()
     env = dict(os.environ, SRDL_DIST_BACKEND="gloo", SRDL_BENCH_NO_CLOCKS="1")
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--workload",
