@@ -18,6 +18,9 @@ constexpr int kBins = 1 << kRadixBits;
 constexpr int kWarps = kThreads / 32;
 constexpr int kWarpChunk = 32 * kItems;
 constexpr int kMaxPasses = 8;  // 64-bit keys
+#ifndef SRDL_SORT_BACKOFF_DEFAULT
+#define SRDL_SORT_BACKOFF_DEFAULT 0
+#endif
 #ifndef SRDL_SORT_ITEMS_DEFAULT
 #define SRDL_SORT_ITEMS_DEFAULT 16
 #endif
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, onesweep_min_blocks<ITEMS>())
     onesweep_pass(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ vals, uint64_t n, int shift,
                   const uint32_t *__restrict__ starts, uint64_t *status, uint64_t epoch, uint32_t *tile_ticket,
                   uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-                  const int *__restrict__ unsorted) {
+                  const int *__restrict__ unsorted, uint32_t backoff_ns) {
     if (unsorted && *unsorted == 0) return;
     constexpr int kI = ITEMS;
     constexpr uint32_t kT = (uint32_t)kThreads * ITEMS;  // keys per tile
@@ -217,6 +220,10 @@ __global__ void __launch_bounds__(kThreads, onesweep_min_blocks<ITEMS>())
             }
             if (done) break;
             t -= j;
+            // no predecessor published since the last window: back off
+            // instead of re-issuing the window loads (spinning tiles take
+            // issue slots from the co-resident tile's ranking)
+            if (j == 0 && backoff_ns) __nanosleep(backoff_ns);
         }
         *(volatile uint64_t *)st = kFlagInc | stamp | (excl + total);
     }
@@ -276,6 +283,15 @@ static int sort_items() {
     return items;
 }
 
+// look-back back-off of the onesweep passes in ns (SRDL_SORT_BACKOFF; A/B knob)
+static uint32_t sort_backoff_ns() {
+    static uint32_t ns = [] {
+        const char *v = getenv("SRDL_SORT_BACKOFF");
+        return v && *v ? (uint32_t)atoi(v) : (uint32_t)SRDL_SORT_BACKOFF_DEFAULT;
+    }();
+    return ns;
+}
+
 // `unsorted` (optional device flag): when it reads 0 every pass returns at
 // once and the keys stay in place, so a caller can skip sorting already
 // ordered input without a host round trip.
@@ -298,6 +314,7 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
                                        (int)onesweep_smem<false, 8>()));
     }
     const int items = sort_items();
+    const uint32_t backoff = sort_backoff_ns();
     const uint64_t tiles = (n + (uint64_t)kThreads * items - 1) / ((uint64_t)kThreads * items);
     Scratch kalt(n * sizeof(uint64_t), s);
     Scratch valt(vals ? n * sizeof(uint32_t) : 16, s);
@@ -324,17 +341,17 @@ void radix_sort(uint64_t *keys, uint32_t *vals, uint64_t n, uint32_t bits, cudaS
         if (items == 8) {
             if (vals)
                 onesweep_pass<true, 8><<<(unsigned)tiles, kThreads, onesweep_smem<true, 8>(), s>>>(
-                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted);
+                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted, backoff);
             else
                 onesweep_pass<false, 8><<<(unsigned)tiles, kThreads, onesweep_smem<false, 8>(), s>>>(
-                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted);
+                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted, backoff);
         } else {
             if (vals)
                 onesweep_pass<true, 16><<<(unsigned)tiles, kThreads, onesweep_smem<true, 16>(), s>>>(
-                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted);
+                    kin, vin, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, vout, unsorted, backoff);
             else
                 onesweep_pass<false, 16><<<(unsigned)tiles, kThreads, onesweep_smem<false, 16>(), s>>>(
-                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted);
+                    kin, nullptr, n, shift, hist + p * kBins, status, epoch, tickets + p, kout, nullptr, unsorted, backoff);
         }
         SRDL_CHECK_LAUNCH();
         std::swap(kin, kout);
