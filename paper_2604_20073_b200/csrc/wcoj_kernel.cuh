@@ -93,6 +93,9 @@ constexpr uint32_t kSegs = SRDL_MAX_SEGS;
 #ifndef SRDL_MERGE_MIN
 #define SRDL_MERGE_MIN 64
 #endif
+#ifndef SRDL_MERGE_SKIP  // merge-path tiles: skip a tile that lies wholly below the other (A/B knob)
+#define SRDL_MERGE_SKIP 0
+#endif
 #ifndef SRDL_MERGE_RATIO
 #define SRDL_MERGE_RATIO 4
 #endif
@@ -506,6 +509,17 @@ __device__ void merge_pair(const srdl_plan &P, const srdl_exec &X, const View &S
         const uint32_t na_tile = min(32u, ea - ia), nb_tile = min(32u, eb - ib);
         const uint32_t alast = __shfl_sync(kFull, av, na_tile - 1);
         const uint32_t blast = __shfl_sync(kFull, bv, nb_tile - 1);
+#if SRDL_MERGE_SKIP
+        // disjoint tiles (warp-uniform test): the lower one has no match
+        if (alast < __shfl_sync(kFull, bv, 0)) {
+            ia += na_tile;
+            continue;
+        }
+        if (blast < __shfl_sync(kFull, av, 0)) {
+            ib += nb_tile;
+            continue;
+        }
+#endif
         const uint32_t m = min(alast, blast);
         uint32_t cnt = 0;  // B tile values < av
 #pragma unroll
