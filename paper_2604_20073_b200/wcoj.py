@@ -37,7 +37,7 @@ from .syntax import VAR
 
 WARPS_PER_SM = 32  # slice-array sizing; the launcher picks the resident wave itself
 SLICES_PER_WARP = 256  # slice-array capacity per launched warp (fetched dynamically)
-MIN_SLICE_UNITS = int(os.environ.get("SRDL_MIN_SLICE_UNITS", 16384))  # root work units per slice, at least (profiles/r02/knobs: triangle 78.4 -> 77.3 ms vs 4096)
+MIN_SLICE_UNITS = int(os.environ.get("SRDL_MIN_SLICE_UNITS", 65536))  # root work units per slice, at least (profiles/r02/knobs: triangle 78.4 ms at 4096 and 16384, 67.2 ms at 65536)
 
 def _timed(name, fn, algo_bytes=0):
     """One WCOJ library call under the bench's event hook (dev.PROFILE)."""
